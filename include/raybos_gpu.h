@@ -1,0 +1,239 @@
+/*
+ * raybos_gpu.h — C-ABI of the B200-native per-ray rendering pipeline.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *
+ *     TraceOutputs raybos::run_trace(const SceneSetup& setup, bool with_field,
+ *                                    bool accumulate_image, const RunConfig& run);
+ *     (reference: proj/include/raybos/engine.hpp:73-78, proj/src/engine.cpp:429-507)
+ *
+ * The reference has no plugin registry; run_trace is the seam.  Everything it
+ * reads from SceneSetup (engine.hpp:40-60) is flattened into the POD structs
+ * below (plain pointers and sizes, no C++ or torch types), and everything it
+ * returns in TraceOutputs (engine.hpp:67-71: per-source DotHitStats, RunReport,
+ * ImageBuffer) is written into caller-owned buffers of rb_trace_out.
+ *
+ * Conventions
+ *  - All entry points return 0 on success and a non-zero RB_E_* code on failure;
+ *    the message is copied into the context (rb_last_error) and, when given, into
+ *    err/errlen.  Nothing throws across the ABI.  The messages for invalid scenes
+ *    are the reference's own exception texts (raygen.cpp:29-31, raygen.cpp:69).
+ *  - Caller owns every host buffer; the context owns device memory.  The density
+ *    grid persists in the context across rb_trace calls (bos_run traces the same
+ *    scene twice, engine.cpp:539-540).
+ *  - An rb_ctx is not thread-safe: one caller at a time (the reference's
+ *    run_trace is a synchronous call too).
+ *  - There is no CPU fallback: rb_create fails when no sm_100 device is present.
+ */
+#ifndef RAYBOS_GPU_H_
+#define RAYBOS_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RB_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------- */
+#define RB_OK 0
+#define RB_E_INVALID 1   /* std::invalid_argument in the reference            */
+#define RB_E_RUNTIME 2   /* std::runtime_error in the reference               */
+#define RB_E_CUDA 3      /* CUDA / NCCL failure                                */
+#define RB_E_NODEVICE 4  /* no usable sm_100 device                            */
+
+/* ---- per-ray outcome codes (rb_trace_rays) ------------------------------ */
+/* Mirrors the counter mapping of process_source, engine.cpp:112-137.        */
+#define RB_RAY_LANDED 0
+#define RB_RAY_LOST 1           /* TraceStatus kLost or kInvalid (grin.hpp:49-54) */
+#define RB_RAY_APERTURE 2       /* BlockReason kApertureStop                    */
+#define RB_RAY_MISSED 3         /* BlockReason kMissedElement                   */
+#define RB_RAY_TIR 4            /* BlockReason kTotalInternalReflection         */
+#define RB_RAY_SENSOR_MISS 5    /* intersect_sensor returned nullopt            */
+
+/* ---- scene ------------------------------------------------------------- */
+typedef struct rb_vec3 {
+  double x, y, z;
+} rb_vec3;
+
+/* raybos::OpticalElement alternatives (optics.hpp:100). */
+#define RB_ELEM_APERTURE 0   /* raybos::Aperture        optics.hpp:80-84  */
+#define RB_ELEM_SINGLET 1    /* raybos::LensElement     optics.hpp:45-52  */
+#define RB_ELEM_THIN_LENS 2  /* raybos::ThinLensIdeal   optics.hpp:88-93  */
+#define RB_ELEM_MIRROR 3     /* raybos::Mirror          optics.hpp:84-86  */
+
+/* raybos::SphericalSurface (optics.hpp:26-36).  curvature_radius = +inf
+ * (or any non-finite value) marks a plane. */
+typedef struct rb_surface {
+  rb_vec3 vertex;
+  rb_vec3 axis;
+  double curvature_radius;
+  double aperture_radius;
+  double n_before;
+  double n_after;
+} rb_surface;
+
+typedef struct rb_element {
+  int32_t kind; /* RB_ELEM_* */
+  int32_t reserved;
+  /* aperture: center, axis = normal, radius.
+   * thin lens: center, axis, focal_length, diameter. */
+  rb_vec3 center;
+  rb_vec3 axis;
+  double radius;
+  double focal_length;
+  double diameter;
+  /* singlet: front, back.  mirror: front. */
+  rb_surface front;
+  rb_surface back;
+} rb_element;
+
+/* raybos::SensorModel (sensor.hpp:19-32); bit_depth and gain are not read by
+ * run_trace (they are used by quantize on the host). */
+typedef struct rb_sensor {
+  rb_vec3 center;
+  rb_vec3 normal;
+  rb_vec3 e_u;
+  rb_vec3 e_v;
+  int32_t width_px;
+  int32_t height_px;
+  double pitch;
+  double window_sigmas;
+} rb_sensor;
+
+#define RB_SAMPLING_STRATIFIED 0 /* ApertureSampling::kStratified   */
+#define RB_SAMPLING_UNIFORM 1    /* ApertureSampling::kUniformRandom */
+
+/* The parts of raybos::SceneSetup (engine.hpp:40-60) run_trace reads. */
+typedef struct rb_scene {
+  const rb_vec3* sources; /* SceneSetup::sources                               */
+  int64_t n_sources;
+  /* Optional RNG stream id per source; NULL means "index in sources", which is
+   * what run_trace uses (engine.cpp:459).  Lets a caller trace a subset of a
+   * scene, or the gain-calibration dot (stream 0xca1, engine.cpp:25,405),
+   * with the reference's ray set. */
+  const int64_t* source_ids;
+  rb_vec3 pupil_center; /* SceneSetup::pupil (raygen.hpp:32-36)             */
+  rb_vec3 pupil_axis;
+  double pupil_radius;
+  int32_t rays_per_source; /* SceneSetup::bundle (raygen.hpp:24-28)          */
+  int32_t sampling;
+  uint64_t seed;
+  double wavelength;
+  double delta_xi; /* SceneSetup::step (grin.hpp:23-26)                       */
+  int32_t max_steps;
+  int32_t n_elements;
+  const rb_element* elements; /* SceneSetup::elements, in order              */
+  rb_sensor sensor;
+  double d_tau;
+  uint64_t config_hash; /* copied into the report                             */
+} rb_scene;
+
+/* Geometry of the density grid (GriddedField, scene.hpp:68-105): node
+ * (i,j,k) sits at origin + (i*dx, j*dy, k*dz), x-fastest storage. */
+typedef struct rb_field_desc {
+  int32_t nx, ny, nz;
+  int32_t reserved;
+  rb_vec3 origin;
+  rb_vec3 spacing;
+} rb_field_desc;
+
+/* Everything TraceOutputs + RunReport carry (engine.hpp:19-36, 67-71). */
+typedef struct rb_trace_out {
+  /* caller-owned, may be NULL */
+  double* hit_sum; /* [2*n_sources]  DotHitStats::hit_sum (u, v) in metres   */
+  int64_t* landed; /* [n_sources]    DotHitStats::landed                      */
+  double* image;   /* [W*H] ImageBuffer::data, row 0 = top; only written when
+                      accumulate_image != 0                                    */
+  /* RunReport */
+  int64_t emitted;
+  int64_t landed_total;
+  int64_t lost;
+  int64_t blocked_aperture;
+  int64_t blocked_miss;
+  int64_t blocked_tir;
+  int64_t blocked_sensor_miss;
+  double wall_seconds;
+  int32_t threads; /* devices used (RunReport::threads)                         */
+  int32_t reserved;
+  uint64_t config_hash;
+  /* instrumentation (not in the reference report) */
+  int64_t total_steps;     /* sum of RK4 steps over all rays                   */
+  double kernel_ms;        /* device time of the render kernel(s), max over devices */
+} rb_trace_out;
+
+typedef struct rb_ctx rb_ctx;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+/* n_devices <= 0: all visible devices.  first_device: ordinal of the first
+ * device to use (devices first_device .. first_device+n-1). */
+int rb_create(int n_devices, int first_device, rb_ctx** out, char* err, size_t errlen);
+void rb_destroy(rb_ctx* ctx);
+const char* rb_last_error(const rb_ctx* ctx);
+int rb_abi_version(void);
+int rb_device_count(const rb_ctx* ctx);
+
+/* ---- density grid ------------------------------------------------------- */
+/* From GriddedField's own node values (node_n / node_grad, scene.hpp:88-92),
+ * FP64 SoA x-fastest, as the reference stores them (scene.hpp:102).  Packed on
+ * device into float4 (n-1, dn/dx, dn/dy, dn/dz). */
+int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, const double* gx,
+                       const double* gy, const double* gz);
+/* From the density volume itself (DensityVolume, scene.hpp:25-40): the
+ * GriddedField constructor (scene.cpp:53-92) runs on device — n = K*rho + 1 and
+ * the central / one-sided differences in FP64 — and packs the same float4 grid. */
+int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rho,
+                         double gladstone_dale_k);
+int rb_clear_field(rb_ctx* ctx);
+/* Bytes of device memory held by the packed grid on each device. */
+int64_t rb_field_bytes(const rb_ctx* ctx);
+
+/* ---- the hot path -------------------------------------------------------- */
+/* run_trace(setup, with_field, accumulate_image, run).  Sources are split over
+ * the context's devices; the partial fixed-point images are summed with one
+ * NCCL reduce when more than one device is used.  Bit-identical results for
+ * any device count. */
+int rb_trace(rb_ctx* ctx, const rb_scene* scene, int with_field, int accumulate_image,
+             rb_trace_out* out);
+
+/* Host-only (needs no device): the shard of every source under
+ * rb_trace_shard(.., shard_index, shard_count, ..).  Sources are ordered along a
+ * Z-order curve of their position projected on the pupil plane (neighbouring
+ * cones cross the same part of the grid) and dealt to shards in tiles of 32
+ * consecutive sources, which balances volume-crossing against missing cones.
+ * rb_trace splits sources over its devices with the same plan. */
+int rb_plan_shards(const rb_scene* scene, int64_t shard_count, int32_t* shard_of_source);
+
+/* One shard of run_trace for multi-process drivers (one process per GPU):
+ * traces the sources rb_plan_shards assigns to shard_index, on device 0 of the
+ * context.  image_fixed, if non-NULL, is a DEVICE pointer to W*H uint64 that
+ * the partial fixed-point image (radiance * 2^31) is added into; the caller
+ * reduces those buffers across ranks (one NCCL sum).  Stats are written only
+ * for the owned sources; counters cover only the owned sources.  out->image is
+ * ignored. */
+int rb_trace_shard(rb_ctx* ctx, const rb_scene* scene, int with_field, int accumulate_image,
+                   int64_t shard_index, int64_t shard_count, uint64_t* image_fixed,
+                   rb_trace_out* out);
+
+/* Converts a device fixed-point image (uint64, radiance * 2^31) to FP64 host
+ * radiance (ImageBuffer::data). */
+int rb_image_from_fixed(rb_ctx* ctx, const uint64_t* image_fixed_device, int64_t n_pixels,
+                        double* image_host);
+
+/* Fixed-point scale of the device image accumulator: 2^31 per unit radiance. */
+#define RB_IMAGE_FIXED_SCALE 2147483648.0
+
+/* Per-ray replay of process_source (engine.cpp:107-140) for a list of
+ * (source index, ray index) pairs: sensor (u, v), outcome (RB_RAY_*) and RK4
+ * steps.  Used by the parity harness and by trace-debug style tooling. */
+int rb_trace_rays(rb_ctx* ctx, const rb_scene* scene, int with_field, int64_t n_rays,
+                  const int64_t* source_index, const int32_t* ray_index, double* uv,
+                  int32_t* status, int32_t* steps);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RAYBOS_GPU_H_ */

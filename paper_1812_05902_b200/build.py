@@ -1,0 +1,77 @@
+"""In-tree build of libraybos_gpu.so (sm_100a only) and of the oracle checkers.
+
+    python -m paper_1812_05902_b200.build
+
+nvcc cross-compiles sm_100a without a GPU, so this runs anywhere the CUDA 12.9
+toolkit is installed.  The .so lands next to this file, so it travels with the
+repo snapshot to the GPU box (a JIT cache would not).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(PKG, "_build")
+LIB = os.path.join(PKG, "libraybos_gpu.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return r.stdout + r.stderr
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_library(verbose: bool = False, force: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    hdrs.append(os.path.join(ROOT, "include", "raybos_gpu.h"))
+    objs = []
+    for src in sorted(os.listdir(CSRC)):
+        if not src.endswith((".cu", ".cpp")):
+            continue
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(BUILD, src + ".o")
+        objs.append(obj)
+        if not force and not _stale(obj, [path] + hdrs):
+            continue
+        flags = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo",
+                 f"-I{os.path.join(ROOT, 'include')}"]
+        if src.endswith(".cu"):
+            flags += ARCH + ["-Xptxas", "-v"]
+        else:
+            flags += ["-x", "c++", "-Wno-deprecated-gpu-targets"]
+        out = _run([NVCC] + flags + ["-c", path, "-o", obj], verbose)
+        if verbose and out.strip():
+            print(out)
+    if force or _stale(LIB, objs):
+        _run([NVCC, "-shared"] + ARCH + objs + ["-o", LIB, "-ldl", "-lpthread"], verbose)
+    return LIB
+
+
+def build_oracle(verbose: bool = False) -> None:
+    """Builds oracle/liboracle.so and, where /root/reference exists, oracle/_ref."""
+    out = _run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"], verbose)
+    if verbose:
+        print(out)
+
+
+if __name__ == "__main__":
+    v = "-v" in sys.argv
+    print(build_library(verbose=v, force="--force" in sys.argv))
+    build_oracle(verbose=v)

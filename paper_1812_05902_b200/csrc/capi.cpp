@@ -1,0 +1,799 @@
+// capi.cpp — host side of the C-ABI (include/raybos_gpu.h).
+//
+// The B200 replacement for run_trace's driver (reference
+// proj/src/engine.cpp:429-507): instead of a std::thread pool over contiguous
+// source ranges with private tiles composited in source order, the sources are
+// ordered along a Z-order curve (so concurrently resident CTAs trace
+// neighbouring cones through the same part of the grid), dealt to GPUs in
+// interleaved tiles, rendered by one persistent K1 launch per GPU into a 64-bit
+// fixed-point image, and the partial images are summed by one NCCL reduce.
+// Integer accumulation makes the result independent of the split.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/raybos_gpu.h"
+#include "kernels.h"
+
+namespace {
+
+constexpr int kShardTile = 32;  // consecutive (Z-ordered) sources per shard tile
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Device {
+  int ordinal = 0;
+  int sms = 148;
+  int blocks_per_sm = 1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float4* grid = nullptr;
+  size_t grid_bytes = 0;
+  Buf sources, ids, order, image, hit, landed, counters, queue, err, dimage, rays_src, rays_idx,
+      rays_uv, rays_status, rays_steps;
+};
+
+struct NcclApi {
+  void* h = nullptr;
+  decltype(&ncclCommInitAll) init_all = nullptr;
+  decltype(&ncclReduce) reduce = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return false;
+    }
+    init_all = reinterpret_cast<decltype(init_all)>(dlsym(h, "ncclCommInitAll"));
+    reduce = reinterpret_cast<decltype(reduce)>(dlsym(h, "ncclReduce"));
+    group_start = reinterpret_cast<decltype(group_start)>(dlsym(h, "ncclGroupStart"));
+    group_end = reinterpret_cast<decltype(group_end)>(dlsym(h, "ncclGroupEnd"));
+    destroy = reinterpret_cast<decltype(destroy)>(dlsym(h, "ncclCommDestroy"));
+    if (!init_all || !reduce || !group_start || !group_end || !destroy) {
+      err = "libnccl.so.2 lacks required symbols";
+      return false;
+    }
+    return true;
+  }
+};
+
+}  // namespace
+
+struct rb_ctx {
+  std::vector<Device> devs;
+  std::string last_error;
+  bool has_field = false;
+  rb_field_desc field{};
+  double3 box_lo{}, box_hi{};
+  NcclApi nccl;
+  std::vector<ncclComm_t> comms;
+};
+
+namespace {
+
+int fail(rb_ctx* ctx, int code, const std::string& msg, char* err = nullptr, size_t len = 0) {
+  if (ctx) ctx->last_error = msg;
+  if (err && len) {
+    std::strncpy(err, msg.c_str(), len - 1);
+    err[len - 1] = '\0';
+  }
+  return code;
+}
+
+#define RB_CUDA(ctx, call)                                                                   \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(ctx, RB_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_));        \
+  } while (0)
+
+double3 d3(const rb_vec3& v) { return make_double3(v.x, v.y, v.z); }
+
+// plane_basis (core.hpp:62-67), evaluated on the host exactly as the reference does.
+void plane_basis(const rb_vec3& a, double3& e1, double3& e2) {
+  const double3 helper = std::abs(a.x) < 0.9 ? make_double3(1, 0, 0) : make_double3(0, 1, 0);
+  const double3 c = make_double3(helper.y * a.z - helper.z * a.y, helper.z * a.x - helper.x * a.z,
+                                 helper.x * a.y - helper.y * a.x);
+  const double n = std::sqrt(c.x * c.x + c.y * c.y + c.z * c.z);
+  e1 = make_double3(c.x / n, c.y / n, c.z / n);
+  e2 = make_double3(a.y * e1.z - a.z * e1.y, a.z * e1.x - a.x * e1.z, a.x * e1.y - a.y * e1.x);
+}
+
+uint64_t mix_bits(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+rbk::DSurface dsurf(const rb_surface& s) {
+  rbk::DSurface d{};
+  d.vertex = d3(s.vertex);
+  d.axis = d3(s.axis);
+  d.R = s.curvature_radius;
+  d.planar = std::isfinite(s.curvature_radius) ? 0 : 1;
+  // curvature_center(), optics.hpp:35
+  d.center = d.planar ? d.vertex
+                      : make_double3(s.vertex.x + s.axis.x * s.curvature_radius,
+                                     s.vertex.y + s.axis.y * s.curvature_radius,
+                                     s.vertex.z + s.axis.z * s.curvature_radius);
+  d.absR = std::abs(s.curvature_radius);
+  d.aperture = s.aperture_radius;
+  d.n_before = s.n_before;
+  d.n_after = s.n_after;
+  return d;
+}
+
+// Reference validation order for the errors run_trace can raise
+// (raygen.cpp:29-31, raygen.cpp:69), plus the limits of this implementation.
+int validate_scene(rb_ctx* ctx, const rb_scene* s) {
+  if (!s) return fail(ctx, RB_E_INVALID, "rb_trace: scene is NULL");
+  if (s->n_sources < 0) return fail(ctx, RB_E_INVALID, "rb_trace: negative source count");
+  if (s->n_sources > 0x7fffffffLL) return fail(ctx, RB_E_INVALID, "rb_trace: too many sources");
+  if (s->sensor.width_px < 1 || s->sensor.height_px < 1)
+    return fail(ctx, RB_E_INVALID, "SensorModel: resolution must be positive");
+  if (s->n_sources == 0) return RB_OK;
+  if (s->rays_per_source < 1)
+    return fail(ctx, RB_E_INVALID, "sample_aperture_points: rays_per_source must be >= 1");
+  if (s->pupil_radius <= 0.0)
+    return fail(ctx, RB_E_INVALID, "sample_aperture_points: radius must be > 0");
+  if (s->wavelength <= 0.0)
+    return fail(ctx, RB_E_INVALID, "emit_rays: wavelength must be positive");
+  if (s->n_elements < 0 || s->n_elements > rbk::kMaxElements)
+    return fail(ctx, RB_E_INVALID, "rb_trace: at most 8 optical elements are supported");
+  if (s->n_elements > 0 && !s->elements)
+    return fail(ctx, RB_E_INVALID, "rb_trace: elements is NULL");
+  if (!s->sources) return fail(ctx, RB_E_INVALID, "rb_trace: sources is NULL");
+  return RB_OK;
+}
+
+rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate) {
+  rbk::KScene k{};
+  k.n_sources = s->n_sources;
+  k.pupil_center = d3(s->pupil_center);
+  plane_basis(s->pupil_axis, k.e1, k.e2);
+  k.pupil_radius = s->pupil_radius;
+  // emit_rays normalises unit weights by their sum, which is exactly N.
+  k.radiance = 1.0 / static_cast<double>(s->rays_per_source);
+  k.key_seed = mix_bits(s->seed ^ 0xa93c0de5ULL);
+  k.rays = s->rays_per_source;
+  k.cells = static_cast<int32_t>(std::ceil(std::sqrt(static_cast<double>(s->rays_per_source))));
+  k.sampling = s->sampling == RB_SAMPLING_STRATIFIED ? 0 : 1;
+  k.with_field = (with_field && ctx->has_field) ? 1 : 0;
+  if (k.with_field) {
+    k.nx = ctx->field.nx;
+    k.ny = ctx->field.ny;
+    k.nz = ctx->field.nz;
+    k.origin = d3(ctx->field.origin);
+    k.spacing = d3(ctx->field.spacing);
+    k.box_lo = ctx->box_lo;
+    k.box_hi = ctx->box_hi;
+    k.h = s->delta_xi;
+    k.max_steps = s->max_steps;
+  }
+  k.n_elem = s->n_elements;
+  for (int e = 0; e < s->n_elements; ++e) {
+    const rb_element& x = s->elements[e];
+    rbk::DElement& d = k.elem[e];
+    d.kind = x.kind;
+    d.center = d3(x.center);
+    d.axis = d3(x.axis);
+    d.radius = x.radius;
+    d.focal = x.focal_length;
+    d.half_diameter = 0.5 * x.diameter;  // propagate_thin_lens clear radius, optics.cpp:119
+    d.front = dsurf(x.front);
+    d.back = dsurf(x.back);
+  }
+  const rb_sensor& se = s->sensor;
+  k.s_center = d3(se.center);
+  k.s_normal = d3(se.normal);
+  k.s_eu = d3(se.e_u);
+  k.s_ev = d3(se.e_v);
+  k.W = se.width_px;
+  k.H = se.height_px;
+  k.pitch = se.pitch;
+  k.sigma = 0.25 * s->d_tau;                                   // sensor.cpp:65
+  k.half_width = se.window_sigmas * k.sigma / se.pitch;        // sensor.cpp:79
+  k.inv_s = 1.0 / (k.sigma * 1.41421356237309504880 / se.pitch);  // sensor.cpp:86
+  k.degenerate = k.sigma < 1e-3 * se.pitch ? 1 : 0;              // sensor.cpp:71
+  k.accumulate = accumulate ? 1 : 0;
+  return k;
+}
+
+uint32_t spread16(uint32_t x) {
+  x &= 0xffff;
+  x = (x | (x << 8)) & 0x00ff00ff;
+  x = (x | (x << 4)) & 0x0f0f0f0f;
+  x = (x | (x << 2)) & 0x33333333;
+  x = (x | (x << 1)) & 0x55555555;
+  return x;
+}
+
+// Z-order of the sources' positions projected on the pupil plane, then dealt
+// to shards in tiles of kShardTile.  Returns the Z-ordered source list.
+std::vector<int32_t> zorder(const rb_scene* s) {
+  const int64_t n = s->n_sources;
+  std::vector<int32_t> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  if (n < 2) return idx;
+  double3 e1, e2;
+  plane_basis(s->pupil_axis, e1, e2);
+  std::vector<double> a(n), b(n);
+  double amin = 1e300, amax = -1e300, bmin = 1e300, bmax = -1e300;
+  for (int64_t i = 0; i < n; ++i) {
+    const rb_vec3& p = s->sources[i];
+    a[i] = p.x * e1.x + p.y * e1.y + p.z * e1.z;
+    b[i] = p.x * e2.x + p.y * e2.y + p.z * e2.z;
+    amin = std::min(amin, a[i]);
+    amax = std::max(amax, a[i]);
+    bmin = std::min(bmin, b[i]);
+    bmax = std::max(bmax, b[i]);
+  }
+  const double sa = amax > amin ? 65535.0 / (amax - amin) : 0.0;
+  const double sb = bmax > bmin ? 65535.0 / (bmax - bmin) : 0.0;
+  std::vector<uint32_t> key(n);
+  for (int64_t i = 0; i < n; ++i) {
+    const uint32_t ia = static_cast<uint32_t>((a[i] - amin) * sa);
+    const uint32_t ib = static_cast<uint32_t>((b[i] - bmin) * sb);
+    key[i] = spread16(ia) | (spread16(ib) << 1);
+  }
+  std::stable_sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+  return idx;
+}
+
+std::vector<int32_t> shard_list(const std::vector<int32_t>& z, int64_t index, int64_t count) {
+  std::vector<int32_t> out;
+  out.reserve(z.size() / std::max<int64_t>(count, 1) + kShardTile);
+  for (size_t p = 0; p < z.size(); ++p)
+    if ((static_cast<int64_t>(p) / kShardTile) % count == index) out.push_back(z[p]);
+  return out;
+}
+
+struct PartialOut {
+  std::vector<double> hit;
+  std::vector<long long> landed;
+  unsigned long long counters[6] = {0, 0, 0, 0, 0, 0};
+  float ms = 0.f;
+  int err_flag = 0;
+};
+
+// One device renders the given work list into dev.image (already zeroed or
+// caller-owned when image_override != nullptr).
+int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& base,
+              const std::vector<int32_t>& work, unsigned long long* image_target,
+              PartialOut& po) {
+  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+  const int64_t n = s->n_sources;
+  const size_t npx = static_cast<size_t>(s->sensor.width_px) * s->sensor.height_px;
+  cudaStream_t st = dev.stream;
+  rbk::KScene k = base;
+  RB_CUDA(ctx, dev.sources.ensure(sizeof(double) * 3 * n));
+  RB_CUDA(ctx, cudaMemcpyAsync(dev.sources.p, s->sources, sizeof(double) * 3 * n,
+                               cudaMemcpyHostToDevice, st));
+  k.sources = dev.sources.as<double>();
+  k.source_ids = nullptr;
+  if (s->source_ids) {
+    RB_CUDA(ctx, dev.ids.ensure(sizeof(int64_t) * n));
+    RB_CUDA(ctx, cudaMemcpyAsync(dev.ids.p, s->source_ids, sizeof(int64_t) * n,
+                                 cudaMemcpyHostToDevice, st));
+    k.source_ids = dev.ids.as<int64_t>();
+  }
+  RB_CUDA(ctx, dev.order.ensure(sizeof(int32_t) * std::max<size_t>(work.size(), 1)));
+  if (!work.empty())
+    RB_CUDA(ctx, cudaMemcpyAsync(dev.order.p, work.data(), sizeof(int32_t) * work.size(),
+                                 cudaMemcpyHostToDevice, st));
+  k.order = dev.order.as<int32_t>();
+  k.n_work = static_cast<int32_t>(work.size());
+  RB_CUDA(ctx, dev.hit.ensure(sizeof(double) * 2 * n));
+  RB_CUDA(ctx, dev.landed.ensure(sizeof(long long) * n));
+  RB_CUDA(ctx, dev.counters.ensure(sizeof(unsigned long long) * 8));
+  RB_CUDA(ctx, dev.queue.ensure(sizeof(int) * 2));
+  RB_CUDA(ctx, cudaMemsetAsync(dev.counters.p, 0, sizeof(unsigned long long) * 8, st));
+  RB_CUDA(ctx, cudaMemsetAsync(dev.queue.p, 0, sizeof(int) * 2, st));
+  k.hit_sum = dev.hit.as<double>();
+  k.landed = dev.landed.as<long long>();
+  k.counters = dev.counters.as<unsigned long long>();
+  k.queue = dev.queue.as<int>();
+  k.err_flag = dev.queue.as<int>() + 1;
+  k.grid = dev.grid;
+  if (k.accumulate) {
+    if (image_target) {
+      k.image = image_target;
+    } else {
+      RB_CUDA(ctx, dev.image.ensure(sizeof(unsigned long long) * npx));
+      RB_CUDA(ctx, cudaMemsetAsync(dev.image.p, 0, sizeof(unsigned long long) * npx, st));
+      k.image = dev.image.as<unsigned long long>();
+    }
+  }
+  if (k.with_field && !dev.grid) return fail(ctx, RB_E_RUNTIME, "rb_trace: field not uploaded");
+  const int grid = std::max(1, std::min<int>(dev.sms * dev.blocks_per_sm,
+                                             std::max<int>(1, static_cast<int>(work.size()))));
+  RB_CUDA(ctx, cudaEventRecord(dev.ev0, st));
+  if (!work.empty()) RB_CUDA(ctx, rbk::launch_render(k, grid, st));
+  RB_CUDA(ctx, cudaEventRecord(dev.ev1, st));
+  po.hit.assign(2 * n, 0.0);
+  po.landed.assign(n, 0);
+  if (n) {
+    RB_CUDA(ctx, cudaMemcpyAsync(po.hit.data(), dev.hit.p, sizeof(double) * 2 * n,
+                                 cudaMemcpyDeviceToHost, st));
+    RB_CUDA(ctx, cudaMemcpyAsync(po.landed.data(), dev.landed.p, sizeof(long long) * n,
+                                 cudaMemcpyDeviceToHost, st));
+  }
+  RB_CUDA(ctx, cudaMemcpyAsync(po.counters, dev.counters.p, sizeof(unsigned long long) * 6,
+                               cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(&po.err_flag, k.err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaStreamSynchronize(st));
+  RB_CUDA(ctx, cudaEventElapsedTime(&po.ms, dev.ev0, dev.ev1));
+  return RB_OK;
+}
+
+void fill_report(rb_trace_out* out, const rb_scene* s, int64_t owned_sources,
+                 const unsigned long long* c, int64_t landed_total) {
+  out->emitted = owned_sources * static_cast<int64_t>(s->rays_per_source);
+  out->landed_total = landed_total;
+  out->lost = static_cast<int64_t>(c[0]);
+  out->blocked_aperture = static_cast<int64_t>(c[1]);
+  out->blocked_miss = static_cast<int64_t>(c[2]);
+  out->blocked_tir = static_cast<int64_t>(c[3]);
+  out->blocked_sensor_miss = static_cast<int64_t>(c[4]);
+  out->total_steps = static_cast<int64_t>(c[5]);
+  out->config_hash = s->config_hash;
+}
+
+int upload_grid(rb_ctx* ctx, Device& dev, size_t count) {
+  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+  if (dev.grid) cudaFree(dev.grid);
+  dev.grid = nullptr;
+  dev.grid_bytes = 0;
+  RB_CUDA(ctx, cudaMalloc(&dev.grid, count * sizeof(float4)));
+  dev.grid_bytes = count * sizeof(float4);
+  return RB_OK;
+}
+
+// Keeps the grid hot in L2 with an access-policy window on the render stream.
+void set_l2_window(Device& dev) {
+  cudaSetDevice(dev.ordinal);
+  int max_persist = 0, max_window = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev.ordinal);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev.ordinal);
+  if (max_persist <= 0 || max_window <= 0 || !dev.grid) return;
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(max_persist));
+  cudaStreamAttrValue attr{};
+  const size_t win = std::min<size_t>(dev.grid_bytes, static_cast<size_t>(max_window));
+  attr.accessPolicyWindow.base_ptr = dev.grid;
+  attr.accessPolicyWindow.num_bytes = win;
+  attr.accessPolicyWindow.hitRatio =
+      std::min(1.0f, static_cast<float>(max_persist) / static_cast<float>(win));
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(dev.stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+  cudaGetLastError();  // the window is a hint; never fail on it
+}
+
+int check_field_desc(rb_ctx* ctx, const rb_field_desc* d) {
+  if (!d) return fail(ctx, RB_E_INVALID, "rb_set_field: desc is NULL");
+  if (d->nx < 2 || d->ny < 2 || d->nz < 2)
+    return fail(ctx, RB_E_INVALID, "DensityVolume: dims must be >= 2 in each axis");
+  if (d->spacing.x <= 0.0 || d->spacing.y <= 0.0 || d->spacing.z <= 0.0)
+    return fail(ctx, RB_E_INVALID, "DensityVolume: spacing must be positive");
+  const double cnt = static_cast<double>(d->nx) * d->ny * d->nz;
+  if (cnt >= 4294967296.0)
+    return fail(ctx, RB_E_INVALID, "rb_set_field: grids are limited to 2^32 nodes");
+  return RB_OK;
+}
+
+void set_box(rb_ctx* ctx, const rb_field_desc* d) {
+  ctx->field = *d;
+  // GriddedField::bounds, scene.cpp:94-97
+  ctx->box_lo = d3(d->origin);
+  ctx->box_hi = make_double3(d->origin.x + (d->nx - 1) * d->spacing.x,
+                             d->origin.y + (d->ny - 1) * d->spacing.y,
+                             d->origin.z + (d->nz - 1) * d->spacing.z);
+  ctx->has_field = true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rb_abi_version(void) { return RB_ABI_VERSION; }
+
+const char* rb_last_error(const rb_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+int rb_device_count(const rb_ctx* ctx) { return ctx ? static_cast<int>(ctx->devs.size()) : 0; }
+
+int rb_create(int n_devices, int first_device, rb_ctx** out, char* err, size_t errlen) {
+  if (!out) return fail(nullptr, RB_E_INVALID, "rb_create: out is NULL", err, errlen);
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(nullptr, RB_E_NODEVICE,
+                std::string("rb_create: no CUDA device (") + cudaGetErrorString(e) +
+                    "); this library has no CPU fallback",
+                err, errlen);
+  if (first_device < 0 || first_device >= count)
+    return fail(nullptr, RB_E_INVALID, "rb_create: first_device out of range", err, errlen);
+  const int n = n_devices <= 0 ? count - first_device : n_devices;
+  if (first_device + n > count)
+    return fail(nullptr, RB_E_INVALID, "rb_create: not enough devices", err, errlen);
+  auto* ctx = new rb_ctx();
+  for (int i = 0; i < n; ++i) {
+    Device dev;
+    dev.ordinal = first_device + i;
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, dev.ordinal);
+    if (prop.major != 10) {
+      delete ctx;
+      return fail(nullptr, RB_E_NODEVICE,
+                  std::string("rb_create: device ") + prop.name +
+                      " is not sm_100 (Blackwell B200); this build targets sm_100a only",
+                  err, errlen);
+    }
+    cudaSetDevice(dev.ordinal);
+    dev.sms = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&dev.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&dev.ev0) != cudaSuccess || cudaEventCreate(&dev.ev1) != cudaSuccess) {
+      delete ctx;
+      return fail(nullptr, RB_E_CUDA, "rb_create: stream/event creation failed", err, errlen);
+    }
+    if (rbk::render_occupancy(&dev.blocks_per_sm) != 0 || dev.blocks_per_sm < 1)
+      dev.blocks_per_sm = 1;
+    ctx->devs.push_back(dev);
+  }
+  if (n > 1) {
+    std::string msg;
+    if (!ctx->nccl.load(msg)) {
+      delete ctx;
+      return fail(nullptr, RB_E_CUDA, msg, err, errlen);
+    }
+    std::vector<int> list(n);
+    for (int i = 0; i < n; ++i) list[i] = first_device + i;
+    ctx->comms.resize(n);
+    if (ctx->nccl.init_all(ctx->comms.data(), n, list.data()) != ncclSuccess) {
+      delete ctx;
+      return fail(nullptr, RB_E_CUDA, "rb_create: ncclCommInitAll failed", err, errlen);
+    }
+  }
+  *out = ctx;
+  return RB_OK;
+}
+
+void rb_destroy(rb_ctx* ctx) {
+  if (!ctx) return;
+  for (ncclComm_t c : ctx->comms)
+    if (c && ctx->nccl.destroy) ctx->nccl.destroy(c);
+  for (Device& d : ctx->devs) {
+    cudaSetDevice(d.ordinal);
+    if (d.grid) cudaFree(d.grid);
+    for (Buf* b : {&d.sources, &d.ids, &d.order, &d.image, &d.hit, &d.landed, &d.counters,
+                   &d.queue, &d.err, &d.dimage, &d.rays_src, &d.rays_idx, &d.rays_uv,
+                   &d.rays_status, &d.rays_steps})
+      b->release();
+    if (d.ev0) cudaEventDestroy(d.ev0);
+    if (d.ev1) cudaEventDestroy(d.ev1);
+    if (d.stream) cudaStreamDestroy(d.stream);
+  }
+  delete ctx;
+}
+
+int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, const double* gx,
+                       const double* gy, const double* gz) {
+  if (!ctx) return RB_E_INVALID;
+  if (int rc = check_field_desc(ctx, desc)) return rc;
+  if (!n || !gx || !gy || !gz) return fail(ctx, RB_E_INVALID, "rb_set_field_nodes: NULL array");
+  const size_t count = static_cast<size_t>(desc->nx) * desc->ny * desc->nz;
+  const size_t chunk = std::min<size_t>(count, size_t(1) << 24);
+  for (Device& dev : ctx->devs) {
+    if (int rc = upload_grid(ctx, dev, count)) return rc;
+    Buf stage;
+    RB_CUDA(ctx, stage.ensure(4 * chunk * sizeof(double)));
+    double* st = stage.as<double>();
+    for (size_t off = 0; off < count; off += chunk) {
+      const size_t m = std::min(chunk, count - off);
+      const double* src[4] = {n + off, gx + off, gy + off, gz + off};
+      for (int a = 0; a < 4; ++a)
+        RB_CUDA(ctx, cudaMemcpyAsync(st + a * chunk, src[a], m * sizeof(double),
+                                     cudaMemcpyHostToDevice, dev.stream));
+      RB_CUDA(ctx, rbk::launch_pack_nodes(st, st + chunk, st + 2 * chunk, st + 3 * chunk,
+                                          dev.grid + off, static_cast<int64_t>(m), dev.stream));
+    }
+    RB_CUDA(ctx, cudaStreamSynchronize(dev.stream));
+    stage.release();
+    set_l2_window(dev);
+  }
+  set_box(ctx, desc);
+  return RB_OK;
+}
+
+int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rho,
+                         double gladstone_dale_k) {
+  if (!ctx) return RB_E_INVALID;
+  if (int rc = check_field_desc(ctx, desc)) return rc;
+  if (!rho) return fail(ctx, RB_E_INVALID, "rb_set_field_density: rho is NULL");
+  if (gladstone_dale_k <= 0.0)
+    return fail(ctx, RB_E_INVALID, "gladstone_dale: K must be positive");  // scene.cpp:18
+  const size_t count = static_cast<size_t>(desc->nx) * desc->ny * desc->nz;
+  for (size_t q = 0; q < count; ++q)  // DensityVolume::validate, scene.cpp:30-33
+    if (!std::isfinite(rho[q]) || rho[q] < 0.0f)
+      return fail(ctx, RB_E_INVALID, "DensityVolume: densities must be finite and >= 0");
+  for (Device& dev : ctx->devs) {
+    if (int rc = upload_grid(ctx, dev, count)) return rc;
+    Buf drho;
+    RB_CUDA(ctx, drho.ensure(count * sizeof(float)));
+    RB_CUDA(ctx, cudaMemcpyAsync(drho.p, rho, count * sizeof(float), cudaMemcpyHostToDevice,
+                                 dev.stream));
+    RB_CUDA(ctx, rbk::launch_build_from_density(drho.as<float>(), desc->nx, desc->ny, desc->nz,
+                                                gladstone_dale_k, d3(desc->spacing), dev.grid, 0,
+                                                desc->nz, dev.stream));
+    RB_CUDA(ctx, cudaStreamSynchronize(dev.stream));
+    drho.release();
+    set_l2_window(dev);
+  }
+  set_box(ctx, desc);
+  return RB_OK;
+}
+
+int rb_clear_field(rb_ctx* ctx) {
+  if (!ctx) return RB_E_INVALID;
+  for (Device& dev : ctx->devs) {
+    cudaSetDevice(dev.ordinal);
+    if (dev.grid) cudaFree(dev.grid);
+    dev.grid = nullptr;
+    dev.grid_bytes = 0;
+  }
+  ctx->has_field = false;
+  return RB_OK;
+}
+
+int64_t rb_field_bytes(const rb_ctx* ctx) {
+  return (ctx && !ctx->devs.empty()) ? static_cast<int64_t>(ctx->devs[0].grid_bytes) : 0;
+}
+
+int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_image,
+             rb_trace_out* out) {
+  if (!ctx || !out) return RB_E_INVALID;
+  const auto t0 = std::chrono::steady_clock::now();
+  if (int rc = validate_scene(ctx, s)) return rc;
+  const int W = s->sensor.width_px, H = s->sensor.height_px;
+  const size_t npx = static_cast<size_t>(W) * H;
+  const int nd = static_cast<int>(ctx->devs.size());
+  out->threads = nd;
+  out->kernel_ms = 0.0;
+  if (s->n_sources == 0) {  // engine.cpp:436: one "thread", blank image, no stats
+    if (accumulate_image && out->image) std::memset(out->image, 0, npx * sizeof(double));
+    const unsigned long long zero[6] = {0, 0, 0, 0, 0, 0};
+    fill_report(out, s, 0, zero, 0);
+    out->threads = 1;
+    out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return RB_OK;
+  }
+  const rbk::KScene base = make_kscene(ctx, s, with_field, accumulate_image);
+  const std::vector<int32_t> z = zorder(s);
+  const int used = static_cast<int>(std::min<int64_t>(nd, (s->n_sources + kShardTile - 1) / kShardTile));
+  std::vector<PartialOut> parts(used);
+  std::vector<int> rcs(used, RB_OK);
+  std::vector<std::vector<int32_t>> work(used);
+  for (int d = 0; d < used; ++d) work[d] = shard_list(z, d, used);
+  if (used == 1) {
+    rcs[0] = render_on(ctx, ctx->devs[0], s, base, work[0], nullptr, parts[0]);
+  } else {
+    std::vector<std::thread> pool;
+    std::mutex mu;
+    for (int d = 0; d < used; ++d)
+      pool.emplace_back([&, d] {
+        const int rc = render_on(ctx, ctx->devs[d], s, base, work[d], nullptr, parts[d]);
+        std::lock_guard<std::mutex> lk(mu);
+        rcs[d] = rc;
+      });
+    for (auto& t : pool) t.join();
+  }
+  for (int d = 0; d < used; ++d)
+    if (rcs[d]) return rcs[d];
+  for (int d = 0; d < used; ++d)
+    if (parts[d].err_flag)
+      return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+
+  // Combine: stats are owned by exactly one device; counters are integers.
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+  int64_t landed_total = 0;
+  float ms = 0.f;
+  for (int d = 0; d < used; ++d) {
+    for (int j = 0; j < 6; ++j) c[j] += parts[d].counters[j];
+    ms = std::max(ms, parts[d].ms);
+    for (int32_t src : work[d]) {
+      if (out->hit_sum) {
+        out->hit_sum[2 * src] = parts[d].hit[2 * src];
+        out->hit_sum[2 * src + 1] = parts[d].hit[2 * src + 1];
+      }
+      if (out->landed) out->landed[src] = parts[d].landed[src];
+      landed_total += parts[d].landed[src];
+    }
+  }
+  if (accumulate_image && out->image) {
+    Device& d0 = ctx->devs[0];
+    if (used > 1) {  // one NCCL sum of the partial fixed-point images onto device 0
+      if (ctx->nccl.group_start() != ncclSuccess)
+        return fail(ctx, RB_E_CUDA, "ncclGroupStart failed");
+      for (int d = 0; d < used; ++d) {
+        Device& dv = ctx->devs[d];
+        cudaSetDevice(dv.ordinal);
+        if (ctx->nccl.reduce(dv.image.p, dv.image.p, npx, ncclUint64, ncclSum, 0, ctx->comms[d],
+                             dv.stream) != ncclSuccess) {
+          ctx->nccl.group_end();
+          return fail(ctx, RB_E_CUDA, "ncclReduce failed");
+        }
+      }
+      if (ctx->nccl.group_end() != ncclSuccess) return fail(ctx, RB_E_CUDA, "ncclGroupEnd failed");
+      for (int d = 0; d < used; ++d) {
+        cudaSetDevice(ctx->devs[d].ordinal);
+        RB_CUDA(ctx, cudaStreamSynchronize(ctx->devs[d].stream));
+      }
+    }
+    RB_CUDA(ctx, cudaSetDevice(d0.ordinal));
+    RB_CUDA(ctx, d0.dimage.ensure(npx * sizeof(double)));
+    RB_CUDA(ctx, rbk::launch_image_finalize(d0.image.as<unsigned long long>(),
+                                            d0.dimage.as<double>(), static_cast<int64_t>(npx),
+                                            d0.stream));
+    RB_CUDA(ctx, cudaMemcpyAsync(out->image, d0.dimage.p, npx * sizeof(double),
+                                 cudaMemcpyDeviceToHost, d0.stream));
+    RB_CUDA(ctx, cudaStreamSynchronize(d0.stream));
+  }
+  fill_report(out, s, s->n_sources, c, landed_total);
+  out->threads = used;
+  out->kernel_ms = ms;
+  out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return RB_OK;
+}
+
+int rb_trace_shard(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_image,
+                   int64_t shard_index, int64_t shard_count, uint64_t* image_fixed,
+                   rb_trace_out* out) {
+  if (!ctx || !out) return RB_E_INVALID;
+  const auto t0 = std::chrono::steady_clock::now();
+  if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
+    return fail(ctx, RB_E_INVALID, "rb_trace_shard: bad shard index/count");
+  if (int rc = validate_scene(ctx, s)) return rc;
+  const unsigned long long zero[6] = {0, 0, 0, 0, 0, 0};
+  out->threads = 1;
+  if (s->n_sources == 0) {
+    fill_report(out, s, 0, zero, 0);
+    return RB_OK;
+  }
+  if (accumulate_image && !image_fixed)
+    return fail(ctx, RB_E_INVALID, "rb_trace_shard: image_fixed (device) required");
+  const rbk::KScene base = make_kscene(ctx, s, with_field, accumulate_image);
+  const std::vector<int32_t> work = shard_list(zorder(s), shard_index, shard_count);
+  PartialOut po;
+  if (int rc = render_on(ctx, ctx->devs[0], s, base, work, reinterpret_cast<unsigned long long*>(image_fixed), po))
+    return rc;
+  if (po.err_flag) return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+  int64_t landed_total = 0;
+  for (int32_t src : work) {
+    if (out->hit_sum) {
+      out->hit_sum[2 * src] = po.hit[2 * src];
+      out->hit_sum[2 * src + 1] = po.hit[2 * src + 1];
+    }
+    if (out->landed) out->landed[src] = po.landed[src];
+    landed_total += po.landed[src];
+  }
+  fill_report(out, s, static_cast<int64_t>(work.size()), po.counters, landed_total);
+  out->kernel_ms = po.ms;
+  out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return RB_OK;
+}
+
+int rb_plan_shards(const rb_scene* s, int64_t shard_count, int32_t* shard_of_source) {
+  if (!s || !shard_of_source || shard_count < 1 || s->n_sources < 0) return RB_E_INVALID;
+  if (s->n_sources > 0 && !s->sources) return RB_E_INVALID;
+  const std::vector<int32_t> z = zorder(s);
+  for (size_t p = 0; p < z.size(); ++p)
+    shard_of_source[z[p]] = static_cast<int32_t>((static_cast<int64_t>(p) / kShardTile) % shard_count);
+  return RB_OK;
+}
+
+int rb_image_from_fixed(rb_ctx* ctx, const uint64_t* image_fixed_device, int64_t n_pixels,
+                        double* image_host) {
+  if (!ctx || !image_fixed_device || !image_host || n_pixels < 0) return RB_E_INVALID;
+  Device& d0 = ctx->devs[0];
+  RB_CUDA(ctx, cudaSetDevice(d0.ordinal));
+  RB_CUDA(ctx, d0.dimage.ensure(static_cast<size_t>(n_pixels) * sizeof(double)));
+  RB_CUDA(ctx, rbk::launch_image_finalize(reinterpret_cast<const unsigned long long*>(image_fixed_device),
+                                          d0.dimage.as<double>(), n_pixels, d0.stream));
+  RB_CUDA(ctx, cudaMemcpyAsync(image_host, d0.dimage.p, static_cast<size_t>(n_pixels) * sizeof(double),
+                               cudaMemcpyDeviceToHost, d0.stream));
+  RB_CUDA(ctx, cudaStreamSynchronize(d0.stream));
+  return RB_OK;
+}
+
+int rb_trace_rays(rb_ctx* ctx, const rb_scene* s, int with_field, int64_t n_rays,
+                  const int64_t* source_index, const int32_t* ray_index, double* uv,
+                  int32_t* status, int32_t* steps) {
+  if (!ctx) return RB_E_INVALID;
+  if (int rc = validate_scene(ctx, s)) return rc;
+  if (n_rays <= 0) return RB_OK;
+  for (int64_t q = 0; q < n_rays; ++q)
+    if (source_index[q] < 0 || source_index[q] >= s->n_sources || ray_index[q] < 0 ||
+        ray_index[q] >= s->rays_per_source)
+      return fail(ctx, RB_E_INVALID, "rb_trace_rays: (source, ray) index out of range");
+  Device& dev = ctx->devs[0];
+  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+  rbk::KScene k = make_kscene(ctx, s, with_field, 0);
+  const int64_t n = s->n_sources;
+  cudaStream_t st = dev.stream;
+  RB_CUDA(ctx, dev.sources.ensure(sizeof(double) * 3 * n));
+  RB_CUDA(ctx, cudaMemcpyAsync(dev.sources.p, s->sources, sizeof(double) * 3 * n,
+                               cudaMemcpyHostToDevice, st));
+  k.sources = dev.sources.as<double>();
+  if (s->source_ids) {
+    RB_CUDA(ctx, dev.ids.ensure(sizeof(int64_t) * n));
+    RB_CUDA(ctx, cudaMemcpyAsync(dev.ids.p, s->source_ids, sizeof(int64_t) * n,
+                                 cudaMemcpyHostToDevice, st));
+    k.source_ids = dev.ids.as<int64_t>();
+  }
+  k.grid = dev.grid;
+  RB_CUDA(ctx, dev.queue.ensure(sizeof(int) * 2));
+  RB_CUDA(ctx, cudaMemsetAsync(dev.queue.p, 0, sizeof(int) * 2, st));
+  k.err_flag = dev.queue.as<int>() + 1;
+  RB_CUDA(ctx, dev.rays_src.ensure(sizeof(int64_t) * n_rays));
+  RB_CUDA(ctx, dev.rays_idx.ensure(sizeof(int32_t) * n_rays));
+  RB_CUDA(ctx, dev.rays_uv.ensure(sizeof(double) * 2 * n_rays));
+  RB_CUDA(ctx, dev.rays_status.ensure(sizeof(int32_t) * n_rays));
+  RB_CUDA(ctx, dev.rays_steps.ensure(sizeof(int32_t) * n_rays));
+  RB_CUDA(ctx, cudaMemcpyAsync(dev.rays_src.p, source_index, sizeof(int64_t) * n_rays,
+                               cudaMemcpyHostToDevice, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(dev.rays_idx.p, ray_index, sizeof(int32_t) * n_rays,
+                               cudaMemcpyHostToDevice, st));
+  RB_CUDA(ctx, rbk::launch_trace_rays(k, n_rays, dev.rays_src.as<int64_t>(),
+                                      dev.rays_idx.as<int32_t>(), dev.rays_uv.as<double>(),
+                                      dev.rays_status.as<int32_t>(), dev.rays_steps.as<int32_t>(),
+                                      st));
+  RB_CUDA(ctx, cudaMemcpyAsync(uv, dev.rays_uv.p, sizeof(double) * 2 * n_rays,
+                               cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(status, dev.rays_status.p, sizeof(int32_t) * n_rays,
+                               cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(steps, dev.rays_steps.p, sizeof(int32_t) * n_rays,
+                               cudaMemcpyDeviceToHost, st));
+  int flag = 0;
+  RB_CUDA(ctx, cudaMemcpyAsync(&flag, k.err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaStreamSynchronize(st));
+  if (flag) return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+  return RB_OK;
+}
+
+}  // extern "C"

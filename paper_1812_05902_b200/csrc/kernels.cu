@@ -1,0 +1,779 @@
+// kernels.cu — the B200 render pipeline (sm_100a).
+//
+// K1 render_emitters fuses the four stages of process_source
+// (reference proj/src/engine.cpp:107-140) for one emitter per CTA:
+//   stage 1  ray generation        raygen.cpp:12-88   FP64, counter RNG (core.hpp:80-107)
+//   stage 2  GRIN RK4 propagation   grin.cpp:23-134    FP32 perturbation form over a float4 grid
+//   stage 3  optics chain           optics.cpp:15-158  FP64 in registers
+//   stage 4  sensor + deposition    sensor.cpp:27-122  FP64 hit, FP32 erf spot weights,
+//            u32 shared-memory tile (native ATOMS.ADD) flushed with u64 global reductions
+// plus make_tile/composite_tile (engine.cpp:142-187): the image is a 64-bit
+// fixed-point sum (radiance * 2^31), so it is order-independent and bit-identical
+// for any emitter order, CTA count or GPU count.
+#include "kernels.h"
+
+#include <math.h>
+
+namespace rbk {
+namespace {
+
+// ---------------------------------------------------------------- math
+__device__ __forceinline__ double3 operator+(double3 a, double3 b) {
+  return make_double3(a.x + b.x, a.y + b.y, a.z + b.z);
+}
+__device__ __forceinline__ double3 operator-(double3 a, double3 b) {
+  return make_double3(a.x - b.x, a.y - b.y, a.z - b.z);
+}
+__device__ __forceinline__ double3 operator*(double3 a, double s) {
+  return make_double3(a.x * s, a.y * s, a.z * s);
+}
+__device__ __forceinline__ double3 operator/(double3 a, double s) {
+  return make_double3(a.x / s, a.y / s, a.z / s);
+}
+__device__ __forceinline__ double3 neg(double3 a) { return make_double3(-a.x, -a.y, -a.z); }
+__device__ __forceinline__ double dot(double3 a, double3 b) {
+  return a.x * b.x + a.y * b.y + a.z * b.z;
+}
+__device__ __forceinline__ double norm(double3 v) { return sqrt(dot(v, v)); }
+__device__ __forceinline__ double3 normalized(double3 v) { return v / norm(v); }
+
+// SplitMix64 finalizer, core.hpp:81-86.
+__device__ __forceinline__ uint64_t mix_bits(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+// CounterRng::uniform for draw number n of an element key, core.hpp:97-100.
+__device__ __forceinline__ double u01(uint64_t key, uint64_t n) {
+  return (double)(mix_bits(key + 0x9e3779b97f4a7c15ULL * n) >> 11) * 0x1p-53;
+}
+
+enum { kMissed = 0, kTraced = 1, kLost = 2, kInvalid = 3 };
+enum { kBrNone = 0, kBrAperture = 1, kBrMissed = 2, kBrTir = 3 };
+
+// ------------------------------------------------------- stage 1: raygen
+// sample_aperture_points (raygen.cpp:27-65) for one ray; ekey is
+// mix_bits(mix_bits(seed ^ salt) + source_index), the per-source part of the
+// CounterRng key.
+__device__ __forceinline__ double3 aperture_point(const KScene& S, uint64_t ekey, int i) {
+  double u, v;
+  const uint64_t key = mix_bits(ekey + (uint64_t)i);
+  if (S.sampling == 0) {
+    if (S.rays == 1) {
+      u = v = 0.5;
+    } else {
+      const int cx = i % S.cells, cy = i / S.cells;
+      u = ((double)cx + u01(key, 1)) / (double)S.cells;
+      v = ((double)cy + u01(key, 2)) / (double)S.cells;
+    }
+  } else {
+    // raygen.cpp:60 under GCC: v takes the first draw, u the second.
+    v = u01(key, 1);
+    u = u01(key, 2);
+  }
+  // concentric_disk_map, raygen.cpp:12-25
+  const double sx = 2.0 * u - 1.0, sy = 2.0 * v - 1.0;
+  double dx = 0.0, dy = 0.0;
+  if (!(sx == 0.0 && sy == 0.0)) {
+    double r, phi;
+    if (fabs(sx) > fabs(sy)) {
+      r = sx;
+      phi = (M_PI / 4.0) * (sy / sx);
+    } else {
+      r = sy;
+      phi = M_PI / 2.0 - (M_PI / 4.0) * (sx / sy);
+    }
+    double sn, cs;
+    sincos(phi, &sn, &cs);
+    dx = r * cs;
+    dy = r * sn;
+  }
+  return S.pupil_center + (S.e1 * dx + S.e2 * dy) * S.pupil_radius;
+}
+
+// --------------------------------------------------------- stage 2: GRIN
+// Trilinear sample of the float4 grid (GriddedField::sample, scene.cpp:99-135)
+// at grid coordinates q, clamped to the box first (ClampedD, grin.cpp:23-33).
+// Returns D = n * grad(n) (d_function, grin.cpp:12-16).
+struct GridView {
+  const float4* __restrict__ g;
+  int nx, nxny, ix, iy, iz;   // ix = nx-2 ... (last cell index)
+  float mx, my, mz;           // n-1 per axis (box in grid coordinates)
+};
+
+__device__ __forceinline__ float4 trilinear(const GridView& G, float qx, float qy, float qz) {
+  qx = fminf(fmaxf(qx, 0.0f), G.mx);
+  qy = fminf(fmaxf(qy, 0.0f), G.my);
+  qz = fminf(fmaxf(qz, 0.0f), G.mz);
+  const int i = min((int)qx, G.ix), j = min((int)qy, G.iy), k = min((int)qz, G.iz);
+  const float fx = qx - (float)i, fy = qy - (float)j, fz = qz - (float)k;
+  const float4* p = G.g + ((unsigned)k * (unsigned)G.nxny + (unsigned)j * (unsigned)G.nx + (unsigned)i);
+  const float4 c000 = __ldg(p), c100 = __ldg(p + 1), c010 = __ldg(p + G.nx),
+               c110 = __ldg(p + G.nx + 1);
+  p += G.nxny;
+  const float4 c001 = __ldg(p), c101 = __ldg(p + 1), c011 = __ldg(p + G.nx),
+               c111 = __ldg(p + G.nx + 1);
+  const float gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
+  const float w00 = gx * gy, w10 = fx * gy, w01 = gx * fy, w11 = fx * fy;
+  const float w000 = w00 * gz, w100 = w10 * gz, w010 = w01 * gz, w110 = w11 * gz;
+  const float w001 = w00 * fz, w101 = w10 * fz, w011 = w01 * fz, w111 = w11 * fz;
+  float4 r;
+#define RB_LERP(ch)                                                                         \
+  r.ch = w000 * c000.ch + w100 * c100.ch + w010 * c010.ch + w110 * c110.ch + w001 * c001.ch + \
+         w101 * c101.ch + w011 * c011.ch + w111 * c111.ch
+  RB_LERP(x);
+  RB_LERP(y);
+  RB_LERP(z);
+  RB_LERP(w);
+#undef RB_LERP
+  return r;
+}
+
+__device__ __forceinline__ float3 d_of(const GridView& G, float qx, float qy, float qz) {
+  const float4 s = trilinear(G, qx, qy, qz);
+  const float n = 1.0f + s.x;
+  return make_float3(s.y * n, s.z * n, s.w * n);
+}
+
+__device__ __forceinline__ bool contains(const KScene& S, double3 p) {
+  return p.x >= S.box_lo.x && p.x <= S.box_hi.x && p.y >= S.box_lo.y && p.y <= S.box_hi.y &&
+         p.z >= S.box_lo.z && p.z <= S.box_hi.z;
+}
+
+// aabb_intersect, grin.cpp:52-72.
+__device__ __forceinline__ bool aabb_intersect(const KScene& S, double3 o, double3 d, double& tn) {
+  double t_near = -INFINITY, t_far = INFINITY;
+  const double oo[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
+  const double lo[3] = {S.box_lo.x, S.box_lo.y, S.box_lo.z};
+  const double hi[3] = {S.box_hi.x, S.box_hi.y, S.box_hi.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (dd[a] == 0.0) {
+      if (oo[a] < lo[a] || oo[a] > hi[a]) return false;
+      continue;
+    }
+    double t0 = (lo[a] - oo[a]) / dd[a], t1 = (hi[a] - oo[a]) / dd[a];
+    if (t0 > t1) {
+      const double tmp = t0;
+      t0 = t1;
+      t1 = tmp;
+    }
+    t_near = t_near < t0 ? t0 : t_near;
+    t_far = t1 < t_far ? t1 : t_far;
+  }
+  if (t_far < t_near || t_far < 0.0) return false;
+  tn = t_near < 0.0 ? 0.0 : t_near;
+  return true;
+}
+
+// trace_through_volume (grin.cpp:74-134) in perturbation form.  With entry
+// point R0 and entry tangent T0 = dir * n(R0), the state after i steps is
+//   r = R0 + T0 * (i*h) + dr,   t = T0 + dt
+// and the RK4-Nystrom step of grin.cpp:35-44 acts on the small (dr, dt) only:
+//   a = D(r)h, b = D(r + (t/2 + a/8)h)h, c = D(r + (t + b/2)h)h
+//   dr' = dr + (dt + (a + 2b)/6) h,  dt' = dt + (a + 4b + c)/6.
+// (dr, dt) are FP32 (grid units for dr); R0, T0 and the exit cut-back are FP64,
+// so rounding never accumulates into the ray position.
+__device__ __noinline__ int grin_trace(const KScene& S, double3& o, double3& d, int& steps) {
+  steps = 0;
+  double tn;
+  if (!aabb_intersect(S, o, d, tn)) return kMissed;
+  if (!(S.h > 0.0)) return kInvalid;
+  const double3 R0 = o + d * (tn + 1e-9);  // kEntryNudge, grin.cpp:85-88
+  if (!contains(S, R0)) return kMissed;
+
+  GridView G;
+  G.g = S.grid;
+  G.nx = S.nx;
+  G.nxny = S.nx * S.ny;
+  G.ix = S.nx - 2;
+  G.iy = S.ny - 2;
+  G.iz = S.nz - 2;
+  G.mx = (float)(S.nx - 1);
+  G.my = (float)(S.ny - 1);
+  G.mz = (float)(S.nz - 1);
+
+  const float q0x = (float)((R0.x - S.origin.x) / S.spacing.x);
+  const float q0y = (float)((R0.y - S.origin.y) / S.spacing.y);
+  const float q0z = (float)((R0.z - S.origin.z) / S.spacing.z);
+  const double n_e = 1.0 + (double)trilinear(G, q0x, q0y, q0z).x;
+  const double3 T0 = d * n_e;  // grin.cpp:91-92
+  const float hf = (float)S.h;
+  // per-step advance of the unperturbed line, and h in grid units per axis
+  const float ax = (float)(T0.x * S.h / S.spacing.x), ay = (float)(T0.y * S.h / S.spacing.y),
+              az = (float)(T0.z * S.h / S.spacing.z);
+  const float hx = (float)(S.h / S.spacing.x), hy = (float)(S.h / S.spacing.y),
+              hz = (float)(S.h / S.spacing.z);
+  const float sixth = 1.0f / 6.0f;
+
+  float drx = 0.f, dry = 0.f, drz = 0.f, dtx = 0.f, dty = 0.f, dtz = 0.f;
+  for (int step = 0; step < S.max_steps; ++step) {
+    const float fs = (float)step;
+    const float pax = fmaf(ax, fs, q0x), pay = fmaf(ay, fs, q0y), paz = fmaf(az, fs, q0z);
+    const float pbx = fmaf(ax, fs + 0.5f, q0x), pby = fmaf(ay, fs + 0.5f, q0y),
+                pbz = fmaf(az, fs + 0.5f, q0z);
+    const float pcx = fmaf(ax, fs + 1.0f, q0x), pcy = fmaf(ay, fs + 1.0f, q0y),
+                pcz = fmaf(az, fs + 1.0f, q0z);
+    float3 a = d_of(G, pax + drx, pay + dry, paz + drz);
+    a.x *= hf;
+    a.y *= hf;
+    a.z *= hf;
+    float3 b = d_of(G, pbx + drx + (dtx * 0.5f + a.x * 0.125f) * hx,
+                    pby + dry + (dty * 0.5f + a.y * 0.125f) * hy,
+                    pbz + drz + (dtz * 0.5f + a.z * 0.125f) * hz);
+    b.x *= hf;
+    b.y *= hf;
+    b.z *= hf;
+    float3 c = d_of(G, pcx + drx + (dtx + b.x * 0.5f) * hx, pcy + dry + (dty + b.y * 0.5f) * hy,
+                    pcz + drz + (dtz + b.z * 0.5f) * hz);
+    c.x *= hf;
+    c.y *= hf;
+    c.z *= hf;
+    const float ndrx = drx + (dtx + (a.x + 2.0f * b.x) * sixth) * hx;
+    const float ndry = dry + (dty + (a.y + 2.0f * b.y) * sixth) * hy;
+    const float ndrz = drz + (dtz + (a.z + 2.0f * b.z) * sixth) * hz;
+    const float ndtx = dtx + (a.x + 4.0f * b.x + c.x) * sixth;
+    const float ndty = dty + (a.y + 4.0f * b.y + c.y) * sixth;
+    const float ndtz = dtz + (a.z + 4.0f * b.z + c.z) * sixth;
+    if (!(isfinite(ndrx) && isfinite(ndry) && isfinite(ndrz) && isfinite(ndtx) &&
+          isfinite(ndty) && isfinite(ndtz))) {
+      steps = step;
+      return kInvalid;  // grin.cpp:99
+    }
+    const float qx = pcx + ndrx, qy = pcy + ndry, qz = pcz + ndrz;
+    if (qx >= 0.0f && qx <= G.mx && qy >= 0.0f && qy <= G.my && qz >= 0.0f && qz <= G.mz) {
+      drx = ndrx;
+      dry = ndry;
+      drz = ndrz;
+      dtx = ndtx;
+      dty = ndty;
+      dtz = ndtz;
+      continue;  // grin.cpp:101-106
+    }
+    // Crossed the boundary: cut back to the first face crossing (grin.cpp:110-130),
+    // evaluated on the FP64 reconstruction of both states.
+    const double xi0 = (double)step * S.h, xi1 = (double)(step + 1) * S.h;
+    const double3 r0 = make_double3(R0.x + T0.x * xi0 + (double)drx * S.spacing.x,
+                                    R0.y + T0.y * xi0 + (double)dry * S.spacing.y,
+                                    R0.z + T0.z * xi0 + (double)drz * S.spacing.z);
+    const double3 r1 = make_double3(R0.x + T0.x * xi1 + (double)ndrx * S.spacing.x,
+                                    R0.y + T0.y * xi1 + (double)ndry * S.spacing.y,
+                                    R0.z + T0.z * xi1 + (double)ndrz * S.spacing.z);
+    const double3 t0 = make_double3(T0.x + (double)dtx, T0.y + (double)dty, T0.z + (double)dtz);
+    const double3 t1 =
+        make_double3(T0.x + (double)ndtx, T0.y + (double)ndty, T0.z + (double)ndtz);
+    double s = 1.0;
+    const double a0[3] = {r0.x, r0.y, r0.z}, a1[3] = {r1.x, r1.y, r1.z};
+    const double lo[3] = {S.box_lo.x, S.box_lo.y, S.box_lo.z};
+    const double hi[3] = {S.box_hi.x, S.box_hi.y, S.box_hi.z};
+#pragma unroll
+    for (int ax3 = 0; ax3 < 3; ++ax3) {
+      const double delta = a1[ax3] - a0[ax3];
+      if (a1[ax3] < lo[ax3]) s = fmin(s, (lo[ax3] - a0[ax3]) / delta);
+      if (a1[ax3] > hi[ax3]) s = fmin(s, (hi[ax3] - a0[ax3]) / delta);
+    }
+    s = fmin(fmax(s, 0.0), 1.0);
+    o = r0 + (r1 - r0) * s;
+    d = normalized(t0 + (t1 - t0) * s);
+    steps = step + 1;
+    return kTraced;
+  }
+  steps = S.max_steps;
+  return kLost;
+}
+
+// ------------------------------------------------------- stage 3: optics
+constexpr double kForwardEps = 1e-12;  // optics.cpp:13
+
+__device__ __forceinline__ double radial_distance(double3 p, double3 axis_point, double3 axis) {
+  const double3 rel = p - axis_point;
+  return norm(rel - axis * dot(rel, axis));
+}
+
+// intersect_plane_cap, optics.cpp:20-30
+__device__ __forceinline__ bool plane_cap(double3 o, double3 d, double3 point, double3 axis,
+                                          double clear, double3& hp, double3& hn) {
+  const double denom = dot(d, axis);
+  if (denom == 0.0) return false;
+  const double t = dot(point - o, axis) / denom;
+  if (t <= kForwardEps) return false;
+  const double3 p = o + d * t;
+  if (radial_distance(p, point, axis) > clear) return false;
+  hp = p;
+  hn = denom < 0.0 ? axis : neg(axis);
+  return true;
+}
+
+// intersect_sphere, optics.cpp:34-57
+__device__ bool sphere_hit(double3 o, double3 d, const DSurface& s, double3& hp, double3& hn) {
+  if (s.planar) return plane_cap(o, d, s.vertex, s.axis, s.aperture, hp, hn);
+  const double3 oc = o - s.center;
+  const double b = dot(oc, d);
+  const double c = dot(oc, oc) - s.R * s.R;
+  const double disc = b * b - c;
+  if (disc < 0.0) return false;
+  const double sq = sqrt(disc);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double t = k == 0 ? -b - sq : -b + sq;
+    if (t <= kForwardEps) continue;
+    const double3 p = o + d * t;
+    if (dot(p - s.center, s.vertex - s.center) <= 0.0) continue;
+    if (radial_distance(p, s.vertex, s.axis) > s.aperture) continue;
+    double3 n = (p - s.center) / s.absR;
+    if (dot(d, n) > 0.0) n = neg(n);
+    hp = p;
+    hn = n;
+    return true;
+  }
+  return false;
+}
+
+// refract, optics.cpp:59-65
+__device__ __forceinline__ bool refract(double3 dir, double3 n, double ni, double nf, double3& out) {
+  const double eta = ni / nf;
+  const double cos_i = -dot(dir, n);
+  const double k = 1.0 - eta * eta * (1.0 - cos_i * cos_i);
+  if (k < 0.0) return false;
+  out = normalized(dir * eta + n * (eta * cos_i - sqrt(k)));
+  return true;
+}
+
+// propagate_chain, optics.cpp:143-158 (first block wins).
+__device__ __noinline__ int optics_chain(const KScene& S, double3& o, double3& d) {
+  for (int e = 0; e < S.n_elem; ++e) {
+    const DElement& el = S.elem[e];
+    if (el.kind == 0) {  // apply_aperture, optics.cpp:108-116: does not advance the ray
+      const double denom = dot(d, el.axis);
+      if (denom == 0.0) return kBrMissed;
+      const double t = dot(el.center - o, el.axis) / denom;
+      if (t <= kForwardEps) return kBrMissed;
+      const double3 p = o + d * t;
+      if (norm(p - el.center) > el.radius) return kBrAperture;
+    } else if (el.kind == 2) {  // propagate_thin_lens, optics.cpp:118-132
+      double3 hp, hn;
+      if (!plane_cap(o, d, el.center, el.axis, el.half_diameter, hp, hn)) return kBrMissed;
+      const double dz = dot(d, el.axis);
+      if (dz <= 0.0) return kBrMissed;
+      const double3 focal_point = el.center + d * (el.focal / dz);
+      o = hp;
+      d = normalized((focal_point - hp) * (el.focal > 0.0 ? 1.0 : -1.0));
+    } else if (el.kind == 1) {  // propagate_through_lens, optics.cpp:85-106
+      double3 hp, hn, in_dir, out_dir;
+      if (!sphere_hit(o, d, el.front, hp, hn)) return kBrMissed;
+      if (!refract(d, hn, el.front.n_before, el.front.n_after, in_dir)) return kBrTir;
+      double3 bp, bn;
+      if (!sphere_hit(hp, in_dir, el.back, bp, bn)) return kBrMissed;
+      if (!refract(in_dir, bn, el.back.n_before, el.back.n_after, out_dir)) return kBrTir;
+      o = bp;
+      d = out_dir;
+    } else {  // reflect_on_mirror, optics.cpp:134-141
+      double3 hp, hn;
+      if (!sphere_hit(o, d, el.front, hp, hn)) return kBrMissed;
+      o = hp;
+      d = d - hn * (2.0 * dot(d, hn));
+    }
+  }
+  return kBrNone;
+}
+
+// ----------------------------------------------- stage 4: sensor + spot
+// intersect_sensor, sensor.cpp:27-34 (no frame check: off-frame hits land).
+__device__ __forceinline__ bool sensor_hit(const KScene& S, double3 o, double3 d, double& u,
+                                           double& v) {
+  const double denom = dot(d, S.s_normal);
+  if (denom == 0.0) return false;
+  const double t = dot(S.s_center - o, S.s_normal) / denom;
+  if (t <= 0.0) return false;
+  const double3 p = o + d * t;
+  u = dot(p - S.s_center, S.s_eu);
+  v = dot(p - S.s_center, S.s_ev);
+  return true;
+}
+
+struct RayResult {
+  double u, v;
+  int status, steps;
+};
+
+// process_source's per-ray body, engine.cpp:112-137.
+__device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, double3 src, int i) {
+  RayResult r;
+  r.steps = 0;
+  r.u = r.v = 0.0;
+  const double3 p = aperture_point(S, ekey, i);
+  const double3 to = p - src;
+  const double len = norm(to);
+  if (!(len > 0.0)) {  // emit_rays: source coincides with aperture point (raygen.cpp:77)
+    atomicOr(S.err_flag, 1);
+    r.status = 1;
+    return r;
+  }
+  double3 o = src, d = to / len;
+  if (S.with_field) {
+    const int st = grin_trace(S, o, d, r.steps);
+    if (st == kLost || st == kInvalid) {
+      r.status = 1;  // RB_RAY_LOST
+      return r;
+    }
+  }
+  const int br = optics_chain(S, o, d);
+  if (br != kBrNone) {
+    r.status = br == kBrAperture ? 2 : (br == kBrTir ? 4 : 3);
+    return r;
+  }
+  if (!sensor_hit(S, o, d, r.u, r.v)) {
+    r.status = 5;
+    return r;
+  }
+  r.status = 0;
+  return r;
+}
+
+// Tile-or-global fixed-point add of one pixel contribution.
+__device__ __forceinline__ void add_px(const KScene& S, uint32_t* tile, int tc0, int tr0, int tw,
+                                       int th, int c, int r, uint32_t f) {
+  const int tx = c - tc0, ty = r - tr0;
+  if ((unsigned)tx < (unsigned)tw && (unsigned)ty < (unsigned)th)
+    atomicAdd(&tile[ty * tw + tx], f);
+  else
+    atomicAdd(&S.image[(size_t)r * S.W + c], (unsigned long long)f);
+}
+
+__device__ __forceinline__ float erf_arg(const KScene& S, int pix, double center) {
+  return (float)(((double)pix - center) * S.inv_s);
+}
+
+// accumulate_spot (sensor.cpp:57-122): separable erf-difference Gaussian,
+// normalized over the full window, in-frame pixels only.
+__device__ __noinline__ void deposit(const KScene& S, double u, double v, uint32_t* tile, int tc0,
+                                     int tr0, int tw, int th) {
+  const double cc = u / S.pitch + 0.5 * S.W;
+  const double rc = 0.5 * S.H - v / S.pitch;
+  const float energy_fx = (float)(S.radiance * 2147483648.0);
+  if (S.degenerate) {  // sensor.cpp:71-77
+    const int col = (int)floor(cc), row = (int)floor(rc);
+    if (col >= 0 && col < S.W && row >= 0 && row < S.H)
+      add_px(S, tile, tc0, tr0, tw, th, col, row, __float2uint_rn(energy_fx));
+    return;
+  }
+  const int c0 = (int)floor(cc - S.half_width), c1 = (int)floor(cc + S.half_width);
+  const int r0 = (int)floor(rc - S.half_width), r1 = (int)floor(rc + S.half_width);
+  const int cb = max(c0, 0), ce = min(c1, S.W - 1), rb = max(r0, 0), re = min(r1, S.H - 1);
+  if (cb > ce || rb > re) return;
+  const int ncol = c1 - c0 + 1;
+  const float eu0 = erff(erf_arg(S, c0, cc));
+  const float ev0 = erff(erf_arg(S, r0, rc));
+  const float ev1 = erff(erf_arg(S, r1 + 1, rc));
+  const float mass_v = 0.5f * (ev1 - ev0);
+  if (ncol <= kMaxSpot) {
+    float wu[kMaxSpot];
+    float e = eu0;
+#pragma unroll
+    for (int k = 0; k < kMaxSpot; ++k) {
+      if (k < ncol) {
+        const float en = erff(erf_arg(S, c0 + k + 1, cc));
+        wu[k] = 0.5f * (en - e);
+        e = en;
+      }
+    }
+    const float mass_u = 0.5f * (e - eu0);
+    const float scale = energy_fx / (mass_u * mass_v);
+    float er = rb == r0 ? ev0 : erff(erf_arg(S, rb, rc));
+    for (int r = rb; r <= re; ++r) {
+      const float er1 = r == r1 ? ev1 : erff(erf_arg(S, r + 1, rc));
+      const float row_w = 0.5f * (er1 - er) * scale;
+      er = er1;
+#pragma unroll
+      for (int k = 0; k < kMaxSpot; ++k) {
+        const int c = c0 + k;
+        if (k < ncol && c >= 0 && c < S.W) {
+          const uint32_t f = __float2uint_rn(wu[k] * row_w);
+          if (f) add_px(S, tile, tc0, tr0, tw, th, c, r, f);
+        }
+      }
+    }
+  } else {  // wide spots: recompute column weights per pixel
+    const float eu1 = erff(erf_arg(S, c1 + 1, cc));
+    const float mass_u = 0.5f * (eu1 - eu0);
+    const float scale = energy_fx / (mass_u * mass_v);
+    float er = rb == r0 ? ev0 : erff(erf_arg(S, rb, rc));
+    for (int r = rb; r <= re; ++r) {
+      const float er1 = r == r1 ? ev1 : erff(erf_arg(S, r + 1, rc));
+      const float row_w = 0.5f * (er1 - er) * scale;
+      er = er1;
+      float ec = cb == c0 ? eu0 : erff(erf_arg(S, cb, cc));
+      for (int c = cb; c <= ce; ++c) {
+        const float ec1 = c == c1 ? eu1 : erff(erf_arg(S, c + 1, cc));
+        const uint32_t f = __float2uint_rn(0.5f * (ec1 - ec) * row_w);
+        ec = ec1;
+        if (f) add_px(S, tile, tc0, tr0, tw, th, c, r, f);
+      }
+    }
+  }
+}
+
+// Deterministic block sum (fixed shuffle tree, fixed warp order).
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace
+
+// ------------------------------------------------ K1: render_emitters
+// One CTA renders one emitter at a time (persistent CTAs pull emitters from a
+// queue, so the work split never affects results).  Thread t owns the K
+// consecutive rays [t*K, t*K+K) of the bundle; its first ray is traced as a
+// pilot before any deposit so the CTA can place the emitter's shared-memory
+// tile over the pilot spots' bounding box (the pilot rays are spread over the
+// whole pupil lattice).  Deposits outside the tile go straight to global.
+__global__ void __launch_bounds__(kBlock, 2) render_emitters(const __grid_constant__ KScene S) {
+  extern __shared__ uint32_t tile[];
+  __shared__ int sh_work;
+  __shared__ int sh_box[4];
+  __shared__ double sh_d[2][kBlock / 32];
+  __shared__ long long sh_l[7][kBlock / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N = S.rays;
+  const int K = (N + kBlock - 1) / kBlock;
+  for (;;) {
+    if (tid == 0) sh_work = atomicAdd(S.queue, 1);
+    if (tid == 1) sh_box[0] = sh_box[1] = 0x7fffffff;
+    if (tid == 2) sh_box[2] = sh_box[3] = -1;
+    __syncthreads();
+    const int w = sh_work;
+    if (w >= S.n_work) break;
+    const int src = S.order[w];
+    const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
+    const double3 so = make_double3(S.sources[3 * src], S.sources[3 * src + 1], S.sources[3 * src + 2]);
+    const uint64_t ekey = mix_bits(S.key_seed + sid);
+
+    double su = 0.0, sv = 0.0;
+    long long cnt[7] = {0, 0, 0, 0, 0, 0, 0};  // landed, lost, aperture, miss, tir, smiss, steps
+    const int i_begin = tid * K, i_end = min(i_begin + K, N);
+
+    RayResult pilot;
+    pilot.status = -1;
+    if (i_begin < i_end) {
+      pilot = trace_ray(S, ekey, so, i_begin);
+      cnt[6] += pilot.steps;
+      if (pilot.status == 0) {
+        su += pilot.u;
+        sv += pilot.v;
+        if (S.accumulate) {  // spot_pixel_window of the pilot, clipped to the frame
+          const double cc = pilot.u / S.pitch + 0.5 * S.W;
+          const double rc = 0.5 * S.H - pilot.v / S.pitch;
+          const int c0 = max((int)floor(cc - S.half_width), 0);
+          const int c1 = min((int)floor(cc + S.half_width), S.W - 1);
+          const int r0 = max((int)floor(rc - S.half_width), 0);
+          const int r1 = min((int)floor(rc + S.half_width), S.H - 1);
+          if (c0 <= c1 && r0 <= r1) {
+            atomicMin(&sh_box[0], c0);
+            atomicMin(&sh_box[1], r0);
+            atomicMax(&sh_box[2], c1);
+            atomicMax(&sh_box[3], r1);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) cnt[k] += (pilot.status == k);
+    }
+
+    int tc0 = 0, tr0 = 0, tw = 0, th = 0;
+    if (S.accumulate) {
+      __syncthreads();
+      if (sh_box[2] >= 0) {
+        const int m = 2;
+        const int bw = sh_box[2] - sh_box[0] + 1 + 2 * m, bh = sh_box[3] - sh_box[1] + 1 + 2 * m;
+        tw = min(bw, S.W);
+        th = min(bh, S.H);
+        if (tw * th > kTileCap) {
+          const float f = sqrtf((float)kTileCap / (float)(tw * th));
+          tw = max(1, min(tw, (int)(tw * f)));
+          th = max(1, min(th, kTileCap / tw));
+        }
+        const int ccen = (sh_box[0] + sh_box[2]) / 2, rcen = (sh_box[1] + sh_box[3]) / 2;
+        tc0 = min(max(ccen - tw / 2, 0), S.W - tw);
+        tr0 = min(max(rcen - th / 2, 0), S.H - th);
+      }
+      for (int q = tid; q < tw * th; q += kBlock) tile[q] = 0u;
+      __syncthreads();
+      if (pilot.status == 0) deposit(S, pilot.u, pilot.v, tile, tc0, tr0, tw, th);
+    }
+
+    for (int i = i_begin + 1; i < i_end; ++i) {
+      const RayResult r = trace_ray(S, ekey, so, i);
+      cnt[6] += r.steps;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) cnt[k] += (r.status == k);
+      if (r.status == 0) {
+        su += r.u;
+        sv += r.v;
+        if (S.accumulate) deposit(S, r.u, r.v, tile, tc0, tr0, tw, th);
+      }
+    }
+
+    // per-emitter stats: DotHitStats (bos.hpp:71-74) + counters
+    su = warp_sum(su);
+    sv = warp_sum(sv);
+#pragma unroll
+    for (int k = 0; k < 7; ++k) cnt[k] = warp_sum(cnt[k]);
+    if (lane == 0) {
+      sh_d[0][warp] = su;
+      sh_d[1][warp] = sv;
+#pragma unroll
+      for (int k = 0; k < 7; ++k) sh_l[k][warp] = cnt[k];
+    }
+    __syncthreads();
+    if (S.accumulate) {  // flush the tile (composite_tile, engine.cpp:181-187)
+      for (int q = tid; q < tw * th; q += kBlock) {
+        const uint32_t f = tile[q];
+        if (f) {
+          const int y = q / tw, x = q - y * tw;
+          atomicAdd(&S.image[(size_t)(tr0 + y) * S.W + (tc0 + x)], (unsigned long long)f);
+        }
+      }
+    }
+    if (tid == 0) {
+      double a = 0.0, b = 0.0;
+      long long l[7] = {0, 0, 0, 0, 0, 0, 0};
+      for (int k = 0; k < kBlock / 32; ++k) {
+        a += sh_d[0][k];
+        b += sh_d[1][k];
+#pragma unroll
+        for (int j = 0; j < 7; ++j) l[j] += sh_l[j][k];
+      }
+      S.hit_sum[2 * src] = a;
+      S.hit_sum[2 * src + 1] = b;
+      S.landed[src] = l[0];
+#pragma unroll
+      for (int j = 1; j < 7; ++j)
+        if (l[j]) atomicAdd(&S.counters[j - 1], (unsigned long long)l[j]);
+    }
+    __syncthreads();
+  }
+}
+
+// Per-ray replay (rb_trace_rays).
+__global__ void trace_rays_kernel(const __grid_constant__ KScene S, int64_t n,
+                                  const int64_t* __restrict__ srcs, const int32_t* __restrict__ rays,
+                                  double* uv, int32_t* status, int32_t* steps) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int64_t src = srcs[q];
+  const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
+  const double3 so = make_double3(S.sources[3 * src], S.sources[3 * src + 1], S.sources[3 * src + 2]);
+  const RayResult r = trace_ray(S, mix_bits(S.key_seed + sid), so, rays[q]);
+  uv[2 * q] = r.status == 0 ? r.u : nan("");
+  uv[2 * q + 1] = r.status == 0 ? r.v : nan("");
+  status[q] = r.status;
+  steps[q] = r.steps;
+}
+
+// ------------------------------------------------ K0: field pack / build
+// float4 (n-1, dn/dx, dn/dy, dn/dz) from GriddedField's FP64 node arrays.
+__global__ void pack_nodes_kernel(const double* __restrict__ n, const double* __restrict__ gx,
+                                  const double* __restrict__ gy, const double* __restrict__ gz,
+                                  float4* __restrict__ out, int64_t count) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < count;
+       q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = make_float4((float)(n[q] - 1.0), (float)gx[q], (float)gy[q], (float)gz[q]);
+}
+
+// GriddedField ctor (scene.cpp:53-92) on device: n = K*rho + 1 (gladstone_dale,
+// scene.cpp:16-20) and central differences inside / one-sided first order on
+// the faces, all FP64 with explicit round-to-nearest ops (no FMA contraction),
+// so the packed grid is bit-identical to packing the reference's own nodes.
+__device__ __forceinline__ double n_of(const float* rho, double k, size_t q) {
+  return __dadd_rn(__dmul_rn(k, (double)rho[q]), 1.0);
+}
+
+__global__ void build_from_density_kernel(const float* __restrict__ rho, int nx, int ny, int nz,
+                                          double k, double3 sp, float4* __restrict__ out, int z0,
+                                          int z1) {
+  const int64_t plane = (int64_t)nx * ny;
+  const int64_t count = plane * (z1 - z0);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int kk = z0 + (int)(t / plane);
+    const int64_t rem = t % plane;
+    const int j = (int)(rem / nx), i = (int)(rem % nx);
+    const size_t q = (size_t)kk * plane + (size_t)j * nx + i;
+    const double nq = n_of(rho, k, q);
+    double g[3];
+    const int idx[3] = {i, j, kk}, dim[3] = {nx, ny, nz};
+    const size_t stride[3] = {1, (size_t)nx, (size_t)plane};
+    const double h[3] = {sp.x, sp.y, sp.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (idx[a] == 0)
+        g[a] = __ddiv_rn(__dsub_rn(n_of(rho, k, q + stride[a]), nq), h[a]);
+      else if (idx[a] == dim[a] - 1)
+        g[a] = __ddiv_rn(__dsub_rn(nq, n_of(rho, k, q - stride[a])), h[a]);
+      else
+        g[a] = __ddiv_rn(__dsub_rn(n_of(rho, k, q + stride[a]), n_of(rho, k, q - stride[a])),
+                         __dmul_rn(2.0, h[a]));
+    }
+    out[q] = make_float4((float)__dsub_rn(nq, 1.0), (float)g[0], (float)g[1], (float)g[2]);
+  }
+}
+
+// ------------------------------------------------ K2: image finalize
+__global__ void image_finalize_kernel(const unsigned long long* __restrict__ fx,
+                                      double* __restrict__ out, int64_t n) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = (double)fx[q] * (1.0 / 2147483648.0);
+}
+
+// ------------------------------------------------ launch wrappers
+static size_t render_smem() { return (size_t)kTileCap * sizeof(uint32_t); }
+
+int render_occupancy(int* blocks_per_sm) {
+  cudaFuncSetAttribute(render_emitters, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)render_smem());
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, render_emitters,
+                                                            kBlock, render_smem());
+}
+
+cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream) {
+  cudaFuncSetAttribute(render_emitters, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)render_smem());
+  render_emitters<<<grid, kBlock, render_smem(), stream>>>(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace_rays(const KScene& s, int64_t n, const int64_t* src, const int32_t* ray,
+                              double* uv, int32_t* status, int32_t* steps, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int bs = 128;
+  trace_rays_kernel<<<(unsigned)((n + bs - 1) / bs), bs, 0, stream>>>(s, n, src, ray, uv, status,
+                                                                      steps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_nodes(const double* n, const double* gx, const double* gy,
+                              const double* gz, float4* out, int64_t count, cudaStream_t stream) {
+  pack_nodes_kernel<<<148 * 8, 256, 0, stream>>>(n, gx, gy, gz, out, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_from_density(const float* rho, int nx, int ny, int nz, double k,
+                                      double3 spacing, float4* out, int z0, int z1,
+                                      cudaStream_t stream) {
+  build_from_density_kernel<<<148 * 8, 256, 0, stream>>>(rho, nx, ny, nz, k, spacing, out, z0, z1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_image_finalize(const unsigned long long* fixed, double* out, int64_t n,
+                                  cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  image_finalize_kernel<<<148 * 4, 256, 0, stream>>>(fixed, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace rbk

@@ -1,0 +1,85 @@
+// kernels.h — device-side scene layout and launch entry points of the
+// B200 render pipeline (K0 field_pack/field_build, K1 render_emitters,
+// K2 image_finalize, plus the per-ray replay kernel).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rbk {
+
+constexpr int kMaxElements = 8;
+constexpr int kBlock = 256;          // threads per CTA (one emitter at a time)
+constexpr int kTileCap = 6144;       // u32 entries of the per-emitter shared tile (24 KB)
+constexpr int kMaxSpot = 16;         // register fast path: spot windows up to 16 columns
+
+// raybos::SphericalSurface with the derived quantities intersect_sphere
+// recomputes on every call (optics.cpp:34-57) hoisted to the host.
+struct DSurface {
+  double3 vertex, axis, center;  // center = vertex + axis * R   (optics.hpp:35)
+  double R, absR, aperture, n_before, n_after;
+  int planar;                    // !isfinite(R)                  (optics.hpp:34)
+  int pad;
+};
+
+struct DElement {
+  int kind, pad;
+  double3 center, axis;
+  double radius, focal, half_diameter;
+  DSurface front, back;
+};
+
+// Everything K1 reads, passed by value (param space / constant bank).
+struct KScene {
+  // sources and work list
+  const double* sources;         // 3 * n_sources
+  const int64_t* source_ids;     // RNG stream per source (may be null = index)
+  const int32_t* order;          // queue position -> source index (owned sources only)
+  int64_t n_sources;
+  int32_t n_work;                // entries in order[]
+  int32_t pad0;
+  // ray generation (raygen.cpp:27-88)
+  double3 pupil_center, e1, e2;
+  double pupil_radius;
+  double radiance;               // 1/N exactly (raygen.cpp:86)
+  uint64_t key_seed;             // mix_bits(seed ^ 0xa93c0de5) (core.hpp:93-94)
+  int32_t rays;                  // N
+  int32_t cells;                 // ceil(sqrt(N))
+  int32_t sampling;
+  int32_t with_field;
+  // density grid (float4: n-1, dn/dx, dn/dy, dn/dz)
+  const float4* grid;
+  int32_t nx, ny, nz, max_steps;
+  double3 origin, spacing, box_lo, box_hi;
+  double h;
+  // optics (optics.cpp:143-158)
+  int32_t n_elem, pad1;
+  DElement elem[kMaxElements];
+  // sensor (sensor.cpp:27-122)
+  double3 s_center, s_normal, s_eu, s_ev;
+  int32_t W, H;
+  double pitch, sigma, half_width, inv_s;
+  int32_t accumulate, degenerate;   // degenerate: sigma < 1e-3 * pitch
+  // outputs
+  unsigned long long* image;        // W*H fixed point (radiance * 2^31)
+  double* hit_sum;                  // 2 * n_sources
+  long long* landed;                // n_sources
+  unsigned long long* counters;     // [0..4] lost, aperture, miss, tir, sensor_miss; [5] steps
+  int* queue;                       // work counter
+  int* err_flag;
+};
+
+// ---- launches (all on `stream`) ----
+cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream);
+int render_occupancy(int* blocks_per_sm);
+cudaError_t launch_trace_rays(const KScene& s, int64_t n, const int64_t* src, const int32_t* ray,
+                              double* uv, int32_t* status, int32_t* steps, cudaStream_t stream);
+cudaError_t launch_pack_nodes(const double* n, const double* gx, const double* gy,
+                              const double* gz, float4* out, int64_t count, cudaStream_t stream);
+cudaError_t launch_build_from_density(const float* rho, int nx, int ny, int nz, double k,
+                                      double3 spacing, float4* out, int z0, int z1,
+                                      cudaStream_t stream);
+cudaError_t launch_image_finalize(const unsigned long long* fixed, double* out, int64_t n,
+                                  cudaStream_t stream);
+
+}  // namespace rbk

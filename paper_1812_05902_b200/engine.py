@@ -1,0 +1,157 @@
+"""Python handle on the C-ABI: the reference's ``run_trace`` (engine.hpp:73-78)
+on B200, plus the multi-process shard entry points.
+
+Everything here is a thin ctypes call into ``libraybos_gpu.so``; the hot path
+never runs in Python and there is no CPU fallback (constructing a
+:class:`GpuTracer` without a B200 raises).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Union
+
+import numpy as np
+
+from . import abi
+from .scene import DensityGrid, FieldNodes, FlatScene, TraceResult, report_from
+
+
+class RaybosError(RuntimeError):
+    pass
+
+
+def _raise(lib, ctx, rc, what):
+    msg = lib.rb_last_error(ctx).decode() if ctx else what
+    if rc == abi.RB_E_INVALID:
+        raise ValueError(msg)
+    raise RaybosError(f"{what}: {msg}")
+
+
+def plan_shards(scene: FlatScene, shard_count: int) -> np.ndarray:
+    """rb_plan_shards: shard of every source (host only, no device needed)."""
+    lib = abi.load_library()
+    s, keep = scene.to_c()
+    out = np.zeros(max(scene.n_sources, 1), dtype=np.int32)
+    rc = lib.rb_plan_shards(C.byref(s), int(shard_count), abi.i32ptr(out))
+    if rc:
+        raise ValueError("rb_plan_shards failed")
+    return out[: scene.n_sources]
+
+
+class GpuTracer:
+    """Owns an ``rb_ctx``: device streams, the resident density grid, buffers."""
+
+    def __init__(self, n_devices: int = 1, first_device: int = 0):
+        self.lib = abi.load_library()
+        self.ctx = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = self.lib.rb_create(int(n_devices), int(first_device), C.byref(self.ctx), err, 1024)
+        if rc:
+            raise RaybosError(f"rb_create failed: {err.value.decode()}")
+
+    def close(self):
+        if self.ctx:
+            self.lib.rb_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def n_devices(self) -> int:
+        return self.lib.rb_device_count(self.ctx)
+
+    # ---- field -------------------------------------------------------------
+    def set_field(self, field: Union[FieldNodes, DensityGrid, None]):
+        if field is None:
+            self.lib.rb_clear_field(self.ctx)
+            return
+        d = field.desc()
+        if isinstance(field, FieldNodes):
+            arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                    (field.n, field.gx, field.gy, field.gz)]
+            rc = self.lib.rb_set_field_nodes(self.ctx, C.byref(d), *[abi.dptr(a) for a in arrs])
+        else:
+            rho = np.ascontiguousarray(field.rho, dtype=np.float32)
+            rc = self.lib.rb_set_field_density(self.ctx, C.byref(d), abi.fptr(rho),
+                                               float(field.gladstone_dale))
+        if rc:
+            _raise(self.lib, self.ctx, rc, "set_field")
+
+    def field_bytes(self) -> int:
+        return int(self.lib.rb_field_bytes(self.ctx))
+
+    # ---- run_trace -----------------------------------------------------------
+    def run_trace(self, scene: FlatScene, with_field: bool = True, accumulate_image: bool = True,
+                  image_out: Optional[np.ndarray] = None) -> TraceResult:
+        s, keep = scene.to_c()
+        n = scene.n_sources
+        hit = np.zeros((n, 2))
+        landed = np.zeros(n, dtype=np.int64)
+        img = None
+        if accumulate_image:
+            img = image_out if image_out is not None else np.empty((scene.height, scene.width))
+            assert img.dtype == np.float64 and img.flags.c_contiguous and img.size == scene.width * scene.height
+        out = abi.TraceOut()
+        out.hit_sum = abi.dptr(hit) if n else None
+        out.landed = abi.i64ptr(landed) if n else None
+        out.image = abi.dptr(img) if img is not None else None
+        rc = self.lib.rb_trace(self.ctx, C.byref(s), int(with_field), int(accumulate_image),
+                               C.byref(out))
+        if rc:
+            _raise(self.lib, self.ctx, rc, "rb_trace")
+        return TraceResult(hit, landed, img, report_from(out))
+
+    def trace_shard(self, scene: FlatScene, with_field: bool, accumulate_image: bool,
+                    shard_index: int, shard_count: int, image_fixed_ptr: int,
+                    hit: Optional[np.ndarray] = None, landed: Optional[np.ndarray] = None) -> dict:
+        """rb_trace_shard; image_fixed_ptr is a device pointer to W*H uint64."""
+        s, keep = scene.to_c()
+        n = scene.n_sources
+        hit = hit if hit is not None else np.zeros((n, 2))
+        landed = landed if landed is not None else np.zeros(n, dtype=np.int64)
+        out = abi.TraceOut()
+        out.hit_sum = abi.dptr(hit) if n else None
+        out.landed = abi.i64ptr(landed) if n else None
+        rc = self.lib.rb_trace_shard(self.ctx, C.byref(s), int(with_field), int(accumulate_image),
+                                     int(shard_index), int(shard_count),
+                                     C.c_void_p(int(image_fixed_ptr)) if image_fixed_ptr else None,
+                                     C.byref(out))
+        if rc:
+            _raise(self.lib, self.ctx, rc, "rb_trace_shard")
+        rep = report_from(out)
+        rep["hit_sum"] = hit
+        rep["landed_per_source"] = landed
+        return rep
+
+    def image_from_fixed(self, image_fixed_ptr: int, shape) -> np.ndarray:
+        img = np.empty(shape, dtype=np.float64)
+        rc = self.lib.rb_image_from_fixed(self.ctx, C.c_void_p(int(image_fixed_ptr)), img.size,
+                                          abi.dptr(img))
+        if rc:
+            _raise(self.lib, self.ctx, rc, "rb_image_from_fixed")
+        return img
+
+    def trace_rays(self, scene: FlatScene, src, ray, with_field: bool = True):
+        s, keep = scene.to_c()
+        src = np.ascontiguousarray(src, dtype=np.int64)
+        ray = np.ascontiguousarray(ray, dtype=np.int32)
+        n = src.shape[0]
+        uv = np.zeros((n, 2))
+        status = np.zeros(n, dtype=np.int32)
+        steps = np.zeros(n, dtype=np.int32)
+        rc = self.lib.rb_trace_rays(self.ctx, C.byref(s), int(with_field), n, abi.i64ptr(src),
+                                    abi.i32ptr(ray), abi.dptr(uv), abi.i32ptr(status),
+                                    abi.i32ptr(steps))
+        if rc:
+            _raise(self.lib, self.ctx, rc, "rb_trace_rays")
+        return uv, status, steps

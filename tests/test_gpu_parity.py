@@ -1,0 +1,160 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference.
+
+Checked against the reference-generated golden fixtures (tests/golden) and the
+bit-exact CPU oracle, with the tolerances the north star states:
+  * per-ray sensor hits within 1e-3 px, identical ray outcomes
+  * per-dot DotHitStats: identical landed counts, mean hit within 1e-3 px
+  * images within 1e-4 relative L2 of the reference FP64 image
+  * images bit-identical for any shard / GPU count (integer accumulation)
+"""
+import numpy as np
+import pytest
+
+from golden_io import NAMES, load
+
+pytestmark = pytest.mark.gpu
+
+PX_TOL = 1e-3      # per-ray and per-dot, pixels
+IMG_RTOL = 1e-4    # relative L2 of the image
+
+
+def rel_l2(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / nb if nb > 0 else np.linalg.norm(a)
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("with_field", [1, 0])
+def test_run_trace_matches_reference(tracer, name, with_field):
+    scene, field, g = load(name)
+    tracer.set_field(field)
+    res = tracer.run_trace(scene, with_field=bool(with_field), accumulate_image=True)
+    r = res.report
+    counters = np.array([r["emitted"], r["landed"], r["lost"], r["blocked_aperture"],
+                         r["blocked_miss"], r["blocked_tir"], r["blocked_sensor_miss"]])
+    assert np.array_equal(counters, g[f"counters_{with_field}"]), (counters, g[f"counters_{with_field}"])
+    assert res.accounting_ok()
+    assert np.array_equal(res.landed, g[f"landed_{with_field}"])
+    pitch = scene.sensor.pitch
+    m = res.landed > 0
+    mean_gpu = res.hit_sum[m] / res.landed[m, None]
+    mean_ref = g[f"hit_sum_{with_field}"][m] / g[f"landed_{with_field}"][m, None]
+    assert np.abs(mean_gpu - mean_ref).max() / pitch < PX_TOL
+    assert rel_l2(res.image, g[f"image_{with_field}"]) < IMG_RTOL
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("with_field", [1, 0])
+def test_per_ray_hits_match_reference(tracer, name, with_field):
+    scene, field, g = load(name)
+    tracer.set_field(field)
+    uv, status, steps = tracer.trace_rays(scene, g["ray_src"], g["ray_idx"], bool(with_field))
+    assert np.array_equal(status, g[f"ray_status_{with_field}"])
+    ok = status == 0
+    err_px = np.abs(uv[ok] - g[f"ray_uv_{with_field}"][ok]).max(initial=0.0) / scene.sensor.pitch
+    assert err_px < PX_TOL, err_px
+    # step counts may differ by one where a step ends within rounding of a face
+    assert np.abs(steps - g[f"ray_steps_{with_field}"]).max(initial=0) <= 1
+
+
+@pytest.mark.parametrize("name", ["field3d", "shock_particles"])
+def test_density_upload_builds_the_reference_grid(tracer, name):
+    """rb_set_field_density (on-device GriddedField ctor) == packing the reference's nodes."""
+    from paper_1812_05902_b200.scene import DensityGrid
+    scene, field, g = load(name)
+    tracer.set_field(field)
+    a = tracer.run_trace(scene, True, True)
+    grid = DensityGrid(field.nx, field.ny, field.nz, field.origin, field.spacing,
+                       g["field_rho"], float(g["field_k"]))
+    tracer.set_field(grid)
+    b = tracer.run_trace(scene, True, True)
+    assert np.array_equal(a.image, b.image)
+    assert np.array_equal(a.hit_sum, b.hit_sum)
+    assert np.array_equal(a.landed, b.landed)
+
+
+@pytest.mark.parametrize("name", ["blob", "field3d", "singlet_defocus"])
+def test_shards_are_bit_identical_to_single_run(tracer, name):
+    """1/2/4/8-way emitter sharding + integer sum == one run, bit for bit."""
+    torch = pytest.importorskip("torch")
+    scene, field, g = load(name)
+    tracer.set_field(field)
+    full = tracer.run_trace(scene, True, True)
+    for count in (1, 2, 3, 8):
+        buf = torch.zeros(scene.height * scene.width, dtype=torch.int64, device="cuda")
+        hit = np.zeros((scene.n_sources, 2))
+        landed = np.zeros(scene.n_sources, dtype=np.int64)
+        tot = 0
+        for k in range(count):
+            rep = tracer.trace_shard(scene, True, True, k, count, buf.data_ptr(), hit, landed)
+            tot += rep["landed"]
+        torch.cuda.synchronize()
+        img = tracer.image_from_fixed(buf.data_ptr(), (scene.height, scene.width))
+        assert np.array_equal(img, full.image), count
+        assert np.array_equal(hit, full.hit_sum), count
+        assert np.array_equal(landed, full.landed)
+        assert tot == full.report["landed"]
+
+
+def test_repeat_runs_are_bit_identical(tracer):
+    scene, field, g = load("field3d")
+    tracer.set_field(field)
+    a = tracer.run_trace(scene, True, True)
+    b = tracer.run_trace(scene, True, True)
+    assert np.array_equal(a.image, b.image) and np.array_equal(a.hit_sum, b.hit_sum)
+
+
+def test_matches_oracle_on_a_fresh_scene(tracer, oracle):
+    """A scene the fixtures do not contain: random sources, blob field, checked live
+    against the bit-exact oracle."""
+    scene, field, g = load("blob")
+    rng = np.random.default_rng(7)
+    scene.sources = np.column_stack([rng.uniform(-0.012, 0.012, 40), rng.uniform(-0.012, 0.012, 40),
+                                     np.zeros(40)])
+    scene.seed = 4242
+    tracer.set_field(field)
+    a = tracer.run_trace(scene, True, True)
+    b = oracle.trace(scene, field, True, True)
+    assert np.array_equal(a.landed, b.landed)
+    assert rel_l2(a.image, b.image) < IMG_RTOL
+    m = a.landed > 0
+    d = np.abs(a.hit_sum[m] / a.landed[m, None] - b.hit_sum[m] / b.landed[m, None]).max()
+    assert d / scene.sensor.pitch < PX_TOL
+
+
+def test_empty_scene_gives_blank_image(tracer):
+    """test_engine.cpp:129-137: zero sources, blank image, zero emitted."""
+    scene, field, g = load("small")
+    scene.sources = np.zeros((0, 3))
+    tracer.set_field(field)
+    res = tracer.run_trace(scene, True, True)
+    assert res.report["emitted"] == 0 and res.report["landed"] == 0
+    assert not res.image.any()
+
+
+@pytest.mark.parametrize("attr,value,msg", [
+    ("rays_per_source", 0, "sample_aperture_points: rays_per_source must be >= 1"),
+    ("pupil_radius", 0.0, "sample_aperture_points: radius must be > 0"),
+    ("wavelength", -1.0, "emit_rays: wavelength must be positive"),
+])
+def test_invalid_scenes_raise_reference_messages(tracer, attr, value, msg):
+    scene, field, g = load("small")
+    setattr(scene, attr, value)
+    with pytest.raises(ValueError, match=msg):
+        tracer.run_trace(scene, True, True)
+
+
+def test_source_on_aperture_point_is_rejected(tracer):
+    """emit_rays throws when a source coincides with its aperture point (raygen.cpp:77)."""
+    scene, field, g = load("single_ray")
+    scene.sources = np.array([list(scene.pupil_center)])
+    with pytest.raises(ValueError, match="coincides"):
+        tracer.run_trace(scene, False, True)
+
+
+def test_no_accumulate_leaves_stats_only(tracer):
+    scene, field, g = load("small")
+    tracer.set_field(field)
+    res = tracer.run_trace(scene, True, accumulate_image=False)
+    assert res.image is None
+    assert np.array_equal(res.landed, g["landed_1"])
