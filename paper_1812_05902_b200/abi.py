@@ -115,7 +115,7 @@ def load_library(path: str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("RAYBOS_LIB") or LIB_PATH
     if not os.path.exists(p):
         raise RuntimeError(
             f"{p} is missing: the CUDA extension must be built (python -c "

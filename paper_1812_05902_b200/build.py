@@ -64,6 +64,18 @@ def build_library(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+PEAKS_LIB = os.path.join(PKG, "libraybos_peaks.so")
+
+
+def build_peaks(verbose: bool = False) -> str:
+    """Measurement microbenchmarks (FP32 FFMA, L2 gather) used by bench.py."""
+    src = os.path.join(PKG, "tools", "peaks.cu")
+    if _stale(PEAKS_LIB, [src]):
+        _run([NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared"] + ARCH +
+             [src, "-o", PEAKS_LIB], verbose)
+    return PEAKS_LIB
+
+
 def build_oracle(verbose: bool = False) -> None:
     """Builds oracle/liboracle.so and, where /root/reference exists, oracle/_ref."""
     out = _run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"], verbose)
@@ -74,4 +86,5 @@ def build_oracle(verbose: bool = False) -> None:
 if __name__ == "__main__":
     v = "-v" in sys.argv
     print(build_library(verbose=v, force="--force" in sys.argv))
+    print(build_peaks(verbose=v))
     build_oracle(verbose=v)

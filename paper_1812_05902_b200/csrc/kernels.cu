@@ -92,196 +92,7 @@ __device__ __forceinline__ double3 aperture_point(const KScene& S, uint64_t ekey
   return S.pupil_center + (S.e1 * dx + S.e2 * dy) * S.pupil_radius;
 }
 
-// --------------------------------------------------------- stage 2: GRIN
-// Trilinear sample of the float4 grid (GriddedField::sample, scene.cpp:99-135)
-// at grid coordinates q, clamped to the box first (ClampedD, grin.cpp:23-33).
-// Returns D = n * grad(n) (d_function, grin.cpp:12-16).
-struct GridView {
-  const float4* __restrict__ g;
-  int nx, nxny, ix, iy, iz;   // ix = nx-2 ... (last cell index)
-  float mx, my, mz;           // n-1 per axis (box in grid coordinates)
-};
-
-__device__ __forceinline__ float4 trilinear(const GridView& G, float qx, float qy, float qz) {
-  qx = fminf(fmaxf(qx, 0.0f), G.mx);
-  qy = fminf(fmaxf(qy, 0.0f), G.my);
-  qz = fminf(fmaxf(qz, 0.0f), G.mz);
-  const int i = min((int)qx, G.ix), j = min((int)qy, G.iy), k = min((int)qz, G.iz);
-  const float fx = qx - (float)i, fy = qy - (float)j, fz = qz - (float)k;
-  const float4* p = G.g + ((unsigned)k * (unsigned)G.nxny + (unsigned)j * (unsigned)G.nx + (unsigned)i);
-  const float4 c000 = __ldg(p), c100 = __ldg(p + 1), c010 = __ldg(p + G.nx),
-               c110 = __ldg(p + G.nx + 1);
-  p += G.nxny;
-  const float4 c001 = __ldg(p), c101 = __ldg(p + 1), c011 = __ldg(p + G.nx),
-               c111 = __ldg(p + G.nx + 1);
-  const float gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
-  const float w00 = gx * gy, w10 = fx * gy, w01 = gx * fy, w11 = fx * fy;
-  const float w000 = w00 * gz, w100 = w10 * gz, w010 = w01 * gz, w110 = w11 * gz;
-  const float w001 = w00 * fz, w101 = w10 * fz, w011 = w01 * fz, w111 = w11 * fz;
-  float4 r;
-#define RB_LERP(ch)                                                                         \
-  r.ch = w000 * c000.ch + w100 * c100.ch + w010 * c010.ch + w110 * c110.ch + w001 * c001.ch + \
-         w101 * c101.ch + w011 * c011.ch + w111 * c111.ch
-  RB_LERP(x);
-  RB_LERP(y);
-  RB_LERP(z);
-  RB_LERP(w);
-#undef RB_LERP
-  return r;
-}
-
-__device__ __forceinline__ float3 d_of(const GridView& G, float qx, float qy, float qz) {
-  const float4 s = trilinear(G, qx, qy, qz);
-  const float n = 1.0f + s.x;
-  return make_float3(s.y * n, s.z * n, s.w * n);
-}
-
-__device__ __forceinline__ bool contains(const KScene& S, double3 p) {
-  return p.x >= S.box_lo.x && p.x <= S.box_hi.x && p.y >= S.box_lo.y && p.y <= S.box_hi.y &&
-         p.z >= S.box_lo.z && p.z <= S.box_hi.z;
-}
-
-// aabb_intersect, grin.cpp:52-72.
-__device__ __forceinline__ bool aabb_intersect(const KScene& S, double3 o, double3 d, double& tn) {
-  double t_near = -INFINITY, t_far = INFINITY;
-  const double oo[3] = {o.x, o.y, o.z}, dd[3] = {d.x, d.y, d.z};
-  const double lo[3] = {S.box_lo.x, S.box_lo.y, S.box_lo.z};
-  const double hi[3] = {S.box_hi.x, S.box_hi.y, S.box_hi.z};
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    if (dd[a] == 0.0) {
-      if (oo[a] < lo[a] || oo[a] > hi[a]) return false;
-      continue;
-    }
-    double t0 = (lo[a] - oo[a]) / dd[a], t1 = (hi[a] - oo[a]) / dd[a];
-    if (t0 > t1) {
-      const double tmp = t0;
-      t0 = t1;
-      t1 = tmp;
-    }
-    t_near = t_near < t0 ? t0 : t_near;
-    t_far = t1 < t_far ? t1 : t_far;
-  }
-  if (t_far < t_near || t_far < 0.0) return false;
-  tn = t_near < 0.0 ? 0.0 : t_near;
-  return true;
-}
-
-// trace_through_volume (grin.cpp:74-134) in perturbation form.  With entry
-// point R0 and entry tangent T0 = dir * n(R0), the state after i steps is
-//   r = R0 + T0 * (i*h) + dr,   t = T0 + dt
-// and the RK4-Nystrom step of grin.cpp:35-44 acts on the small (dr, dt) only:
-//   a = D(r)h, b = D(r + (t/2 + a/8)h)h, c = D(r + (t + b/2)h)h
-//   dr' = dr + (dt + (a + 2b)/6) h,  dt' = dt + (a + 4b + c)/6.
-// (dr, dt) are FP32 (grid units for dr); R0, T0 and the exit cut-back are FP64,
-// so rounding never accumulates into the ray position.
-__device__ __noinline__ int grin_trace(const KScene& S, double3& o, double3& d, int& steps) {
-  steps = 0;
-  double tn;
-  if (!aabb_intersect(S, o, d, tn)) return kMissed;
-  if (!(S.h > 0.0)) return kInvalid;
-  const double3 R0 = o + d * (tn + 1e-9);  // kEntryNudge, grin.cpp:85-88
-  if (!contains(S, R0)) return kMissed;
-
-  GridView G;
-  G.g = S.grid;
-  G.nx = S.nx;
-  G.nxny = S.nx * S.ny;
-  G.ix = S.nx - 2;
-  G.iy = S.ny - 2;
-  G.iz = S.nz - 2;
-  G.mx = (float)(S.nx - 1);
-  G.my = (float)(S.ny - 1);
-  G.mz = (float)(S.nz - 1);
-
-  const float q0x = (float)((R0.x - S.origin.x) / S.spacing.x);
-  const float q0y = (float)((R0.y - S.origin.y) / S.spacing.y);
-  const float q0z = (float)((R0.z - S.origin.z) / S.spacing.z);
-  const double n_e = 1.0 + (double)trilinear(G, q0x, q0y, q0z).x;
-  const double3 T0 = d * n_e;  // grin.cpp:91-92
-  const float hf = (float)S.h;
-  // per-step advance of the unperturbed line, and h in grid units per axis
-  const float ax = (float)(T0.x * S.h / S.spacing.x), ay = (float)(T0.y * S.h / S.spacing.y),
-              az = (float)(T0.z * S.h / S.spacing.z);
-  const float hx = (float)(S.h / S.spacing.x), hy = (float)(S.h / S.spacing.y),
-              hz = (float)(S.h / S.spacing.z);
-  const float sixth = 1.0f / 6.0f;
-
-  float drx = 0.f, dry = 0.f, drz = 0.f, dtx = 0.f, dty = 0.f, dtz = 0.f;
-  for (int step = 0; step < S.max_steps; ++step) {
-    const float fs = (float)step;
-    const float pax = fmaf(ax, fs, q0x), pay = fmaf(ay, fs, q0y), paz = fmaf(az, fs, q0z);
-    const float pbx = fmaf(ax, fs + 0.5f, q0x), pby = fmaf(ay, fs + 0.5f, q0y),
-                pbz = fmaf(az, fs + 0.5f, q0z);
-    const float pcx = fmaf(ax, fs + 1.0f, q0x), pcy = fmaf(ay, fs + 1.0f, q0y),
-                pcz = fmaf(az, fs + 1.0f, q0z);
-    float3 a = d_of(G, pax + drx, pay + dry, paz + drz);
-    a.x *= hf;
-    a.y *= hf;
-    a.z *= hf;
-    float3 b = d_of(G, pbx + drx + (dtx * 0.5f + a.x * 0.125f) * hx,
-                    pby + dry + (dty * 0.5f + a.y * 0.125f) * hy,
-                    pbz + drz + (dtz * 0.5f + a.z * 0.125f) * hz);
-    b.x *= hf;
-    b.y *= hf;
-    b.z *= hf;
-    float3 c = d_of(G, pcx + drx + (dtx + b.x * 0.5f) * hx, pcy + dry + (dty + b.y * 0.5f) * hy,
-                    pcz + drz + (dtz + b.z * 0.5f) * hz);
-    c.x *= hf;
-    c.y *= hf;
-    c.z *= hf;
-    const float ndrx = drx + (dtx + (a.x + 2.0f * b.x) * sixth) * hx;
-    const float ndry = dry + (dty + (a.y + 2.0f * b.y) * sixth) * hy;
-    const float ndrz = drz + (dtz + (a.z + 2.0f * b.z) * sixth) * hz;
-    const float ndtx = dtx + (a.x + 4.0f * b.x + c.x) * sixth;
-    const float ndty = dty + (a.y + 4.0f * b.y + c.y) * sixth;
-    const float ndtz = dtz + (a.z + 4.0f * b.z + c.z) * sixth;
-    if (!(isfinite(ndrx) && isfinite(ndry) && isfinite(ndrz) && isfinite(ndtx) &&
-          isfinite(ndty) && isfinite(ndtz))) {
-      steps = step;
-      return kInvalid;  // grin.cpp:99
-    }
-    const float qx = pcx + ndrx, qy = pcy + ndry, qz = pcz + ndrz;
-    if (qx >= 0.0f && qx <= G.mx && qy >= 0.0f && qy <= G.my && qz >= 0.0f && qz <= G.mz) {
-      drx = ndrx;
-      dry = ndry;
-      drz = ndrz;
-      dtx = ndtx;
-      dty = ndty;
-      dtz = ndtz;
-      continue;  // grin.cpp:101-106
-    }
-    // Crossed the boundary: cut back to the first face crossing (grin.cpp:110-130),
-    // evaluated on the FP64 reconstruction of both states.
-    const double xi0 = (double)step * S.h, xi1 = (double)(step + 1) * S.h;
-    const double3 r0 = make_double3(R0.x + T0.x * xi0 + (double)drx * S.spacing.x,
-                                    R0.y + T0.y * xi0 + (double)dry * S.spacing.y,
-                                    R0.z + T0.z * xi0 + (double)drz * S.spacing.z);
-    const double3 r1 = make_double3(R0.x + T0.x * xi1 + (double)ndrx * S.spacing.x,
-                                    R0.y + T0.y * xi1 + (double)ndry * S.spacing.y,
-                                    R0.z + T0.z * xi1 + (double)ndrz * S.spacing.z);
-    const double3 t0 = make_double3(T0.x + (double)dtx, T0.y + (double)dty, T0.z + (double)dtz);
-    const double3 t1 =
-        make_double3(T0.x + (double)ndtx, T0.y + (double)ndty, T0.z + (double)ndtz);
-    double s = 1.0;
-    const double a0[3] = {r0.x, r0.y, r0.z}, a1[3] = {r1.x, r1.y, r1.z};
-    const double lo[3] = {S.box_lo.x, S.box_lo.y, S.box_lo.z};
-    const double hi[3] = {S.box_hi.x, S.box_hi.y, S.box_hi.z};
-#pragma unroll
-    for (int ax3 = 0; ax3 < 3; ++ax3) {
-      const double delta = a1[ax3] - a0[ax3];
-      if (a1[ax3] < lo[ax3]) s = fmin(s, (lo[ax3] - a0[ax3]) / delta);
-      if (a1[ax3] > hi[ax3]) s = fmin(s, (hi[ax3] - a0[ax3]) / delta);
-    }
-    s = fmin(fmax(s, 0.0), 1.0);
-    o = r0 + (r1 - r0) * s;
-    d = normalized(t0 + (t1 - t0) * s);
-    steps = step + 1;
-    return kTraced;
-  }
-  steps = S.max_steps;
-  return kLost;
-}
+#include "grin.cuh"
 
 // ------------------------------------------------------- stage 3: optics
 constexpr double kForwardEps = 1e-12;  // optics.cpp:13
@@ -341,7 +152,7 @@ __device__ __forceinline__ bool refract(double3 dir, double3 n, double ni, doubl
 }
 
 // propagate_chain, optics.cpp:143-158 (first block wins).
-__device__ __noinline__ int optics_chain(const KScene& S, double3& o, double3& d) {
+__device__ __forceinline__ int optics_chain(const KScene& S, double3& o, double3& d) {
   for (int e = 0; e < S.n_elem; ++e) {
     const DElement& el = S.elem[e];
     if (el.kind == 0) {  // apply_aperture, optics.cpp:108-116: does not advance the ray
@@ -447,7 +258,7 @@ __device__ __forceinline__ float erf_arg(const KScene& S, int pix, double center
 
 // accumulate_spot (sensor.cpp:57-122): separable erf-difference Gaussian,
 // normalized over the full window, in-frame pixels only.
-__device__ __noinline__ void deposit(const KScene& S, double u, double v, uint32_t* tile, int tc0,
+__device__ __forceinline__ void deposit(const KScene& S, double u, double v, uint32_t* tile, int tc0,
                                      int tr0, int tw, int th) {
   const double cc = u / S.pitch + 0.5 * S.W;
   const double rc = 0.5 * S.H - v / S.pitch;
@@ -531,7 +342,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 // pilot before any deposit so the CTA can place the emitter's shared-memory
 // tile over the pilot spots' bounding box (the pilot rays are spread over the
 // whole pupil lattice).  Deposits outside the tile go straight to global.
-__global__ void __launch_bounds__(kBlock, 2) render_emitters(const __grid_constant__ KScene S) {
+__global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __grid_constant__ KScene S) {
   extern __shared__ uint32_t tile[];
   __shared__ int sh_work;
   __shared__ int sh_box[4];
@@ -556,17 +367,19 @@ __global__ void __launch_bounds__(kBlock, 2) render_emitters(const __grid_consta
     long long cnt[7] = {0, 0, 0, 0, 0, 0, 0};  // landed, lost, aperture, miss, tir, smiss, steps
     const int i_begin = tid * K, i_end = min(i_begin + K, N);
 
-    RayResult pilot;
-    pilot.status = -1;
-    if (i_begin < i_end) {
-      pilot = trace_ray(S, ekey, so, i_begin);
-      cnt[6] += pilot.steps;
-      if (pilot.status == 0) {
-        su += pilot.u;
-        sv += pilot.v;
-        if (S.accumulate) {  // spot_pixel_window of the pilot, clipped to the frame
-          const double cc = pilot.u / S.pitch + 0.5 * S.W;
-          const double rc = 0.5 * S.H - pilot.v / S.pitch;
+    // One loop, one trace_ray call site: iteration 0 is the pilot, after which
+    // the CTA places the tile.  __syncwarp() reconverges the lanes after every
+    // ray so a warp never splits into groups running different rays' RK4 loops.
+    int tc0 = 0, tr0 = 0, tw = 0, th = 0;
+    for (int k = 0; k < K; ++k) {
+      const int i = i_begin + k;
+      RayResult r;
+      r.status = -1;
+      if (i < i_end) r = trace_ray(S, ekey, so, i);
+      if (k == 0 && S.accumulate) {  // block-uniform branch
+        if (r.status == 0) {  // spot_pixel_window of the pilot, clipped to the frame
+          const double cc = r.u / S.pitch + 0.5 * S.W;
+          const double rc = 0.5 * S.H - r.v / S.pitch;
           const int c0 = max((int)floor(cc - S.half_width), 0);
           const int c1 = min((int)floor(cc + S.half_width), S.W - 1);
           const int r0 = max((int)floor(rc - S.half_width), 0);
@@ -578,43 +391,35 @@ __global__ void __launch_bounds__(kBlock, 2) render_emitters(const __grid_consta
             atomicMax(&sh_box[3], r1);
           }
         }
-      }
-#pragma unroll
-      for (int k = 0; k < 6; ++k) cnt[k] += (pilot.status == k);
-    }
-
-    int tc0 = 0, tr0 = 0, tw = 0, th = 0;
-    if (S.accumulate) {
-      __syncthreads();
-      if (sh_box[2] >= 0) {
-        const int m = 2;
-        const int bw = sh_box[2] - sh_box[0] + 1 + 2 * m, bh = sh_box[3] - sh_box[1] + 1 + 2 * m;
-        tw = min(bw, S.W);
-        th = min(bh, S.H);
-        if (tw * th > kTileCap) {
-          const float f = sqrtf((float)kTileCap / (float)(tw * th));
-          tw = max(1, min(tw, (int)(tw * f)));
-          th = max(1, min(th, kTileCap / tw));
+        __syncthreads();
+        if (sh_box[2] >= 0) {
+          const int m = 2;
+          const int bw = sh_box[2] - sh_box[0] + 1 + 2 * m, bh = sh_box[3] - sh_box[1] + 1 + 2 * m;
+          tw = min(bw, S.W);
+          th = min(bh, S.H);
+          if (tw * th > kTileCap) {
+            const float f = sqrtf((float)kTileCap / (float)(tw * th));
+            tw = max(1, min(tw, (int)(tw * f)));
+            th = max(1, min(th, kTileCap / tw));
+          }
+          const int ccen = (sh_box[0] + sh_box[2]) / 2, rcen = (sh_box[1] + sh_box[3]) / 2;
+          tc0 = min(max(ccen - tw / 2, 0), S.W - tw);
+          tr0 = min(max(rcen - th / 2, 0), S.H - th);
         }
-        const int ccen = (sh_box[0] + sh_box[2]) / 2, rcen = (sh_box[1] + sh_box[3]) / 2;
-        tc0 = min(max(ccen - tw / 2, 0), S.W - tw);
-        tr0 = min(max(rcen - th / 2, 0), S.H - th);
+        for (int q = tid; q < tw * th; q += kBlock) tile[q] = 0u;
+        __syncthreads();
       }
-      for (int q = tid; q < tw * th; q += kBlock) tile[q] = 0u;
-      __syncthreads();
-      if (pilot.status == 0) deposit(S, pilot.u, pilot.v, tile, tc0, tr0, tw, th);
-    }
-
-    for (int i = i_begin + 1; i < i_end; ++i) {
-      const RayResult r = trace_ray(S, ekey, so, i);
-      cnt[6] += r.steps;
+      if (r.status >= 0) {
+        cnt[6] += r.steps;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) cnt[k] += (r.status == k);
-      if (r.status == 0) {
-        su += r.u;
-        sv += r.v;
-        if (S.accumulate) deposit(S, r.u, r.v, tile, tc0, tr0, tw, th);
+        for (int j = 0; j < 6; ++j) cnt[j] += (r.status == j);
+        if (r.status == 0) {
+          su += r.u;
+          sv += r.v;
+          if (S.accumulate) deposit(S, r.u, r.v, tile, tc0, tr0, tw, th);
+        }
       }
+      __syncwarp();
     }
 
     // per-emitter stats: DotHitStats (bos.hpp:71-74) + counters

@@ -9,7 +9,14 @@
 namespace rbk {
 
 constexpr int kMaxElements = 8;
-constexpr int kBlock = 256;          // threads per CTA (one emitter at a time)
+#ifndef RB_BLOCK
+#define RB_BLOCK 256
+#endif
+#ifndef RB_MINB
+#define RB_MINB 3
+#endif
+constexpr int kBlock = RB_BLOCK;     // threads per CTA (one emitter at a time)
+constexpr int kMinBlocks = RB_MINB;  // resident CTAs per SM the register budget targets
 constexpr int kTileCap = 6144;       // u32 entries of the per-emitter shared tile (24 KB)
 constexpr int kMaxSpot = 16;         // register fast path: spot windows up to 16 columns
 

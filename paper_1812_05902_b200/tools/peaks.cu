@@ -1,0 +1,111 @@
+// peaks.cu — measurement infrastructure (not on the render path).
+//
+// MEASURED_PEAKS.json carries only HBM copy bandwidth and cuBLAS bf16; the
+// render kernel is bound by FP32 CUDA-core arithmetic over cache-resident
+// gathers, so bench.py measures those two roofs on the box:
+//   * FP32 FFMA throughput (register-operand and immediate-operand forms)
+//   * L2-resident float4 gather bandwidth (LDG.128 over a 64 MiB working set)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+namespace {
+
+template <bool kImm>
+__global__ void __launch_bounds__(256) ffma_kernel(float* out, float b, float c, int iters) {
+  float a0 = threadIdx.x * 1e-3f, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+        a6 = a0 + 6, a7 = a0 + 7;
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i) {
+    if (kImm) {
+      a0 = fmaf(a0, 0.999f, 1e-3f); a1 = fmaf(a1, 0.999f, 1e-3f); a2 = fmaf(a2, 0.999f, 1e-3f);
+      a3 = fmaf(a3, 0.999f, 1e-3f); a4 = fmaf(a4, 0.999f, 1e-3f); a5 = fmaf(a5, 0.999f, 1e-3f);
+      a6 = fmaf(a6, 0.999f, 1e-3f); a7 = fmaf(a7, 0.999f, 1e-3f);
+    } else {
+      a0 = fmaf(a0, b, c); a1 = fmaf(a1, b, c); a2 = fmaf(a2, b, c); a3 = fmaf(a3, b, c);
+      a4 = fmaf(a4, b, c); a5 = fmaf(a5, b, c); a6 = fmaf(a6, b, c); a7 = fmaf(a7, b, c);
+    }
+  }
+  const float s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678f) out[threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) gather_kernel(const float4* __restrict__ p, size_t n,
+                                                     int reps, float* out) {
+  float acc = 0.f;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < reps; ++r)
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+      const float4 v = __ldg(p + q);
+      acc += v.x + v.y + v.z + v.w;
+    }
+  if (acc == 12345.678f) out[0] = acc;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Best-of-5 FP32 FFMA throughput in TFLOP/s (2 flops per FMA).  mode 0:
+// register operands, 1: immediate operands.
+double rbp_ffma_tflops(int device, int mode) {
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float* out = nullptr;
+  cudaMalloc(&out, 1024 * sizeof(float));
+  const int blocks = sms * 8, threads = 256, iters = 1 << 14;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(e0);
+    if (mode) ffma_kernel<true><<<blocks, threads>>>(out, 0.999f, 1e-3f, iters);
+    else ffma_kernel<false><<<blocks, threads>>>(out, 0.999f, 1e-3f, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 8.0 * iters * (double)blocks * threads;
+    if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? best : -1.0;
+}
+
+// Best-of-5 read bandwidth (GB/s) of LDG.128 over an L2-resident working set.
+double rbp_l2_gather_gbs(int device, double mib) {
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const size_t n = (size_t)(mib * 1024 * 1024) / sizeof(float4);
+  float4* p = nullptr;
+  float* out = nullptr;
+  cudaMalloc(&p, n * sizeof(float4));
+  cudaMalloc(&out, sizeof(float));
+  cudaMemset(p, 0, n * sizeof(float4));
+  const int reps = 20;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(e0);
+    gather_kernel<<<sms * 8, 256>>>(p, n, reps, out);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0) best = std::max(best, (double)n * sizeof(float4) * reps / (ms * 1e-3) / 1e9);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(p);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? best : -1.0;
+}
+
+}  // extern "C"
