@@ -194,6 +194,15 @@ rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, in
   k.rays = s->rays_per_source;
   k.cells = static_cast<int32_t>(std::ceil(std::sqrt(static_cast<double>(s->rays_per_source))));
   k.sampling = s->sampling == RB_SAMPLING_STRATIFIED ? 0 : 1;
+  {
+    const int rows = (s->rays_per_source + k.cells - 1) / k.cells;
+    k.patch_px = (k.cells + 7) / 8;
+    k.patch_count = k.patch_px * ((rows + 3) / 4);
+    const int warps = rbk::kBlock / 32;
+    int st = std::max(1, k.patch_count / warps);
+    while (std::gcd(st, k.patch_count) != 1) ++st;
+    k.patch_stride = st % std::max(1, k.patch_count) == 0 ? 1 : st;
+  }
   k.with_field = (with_field && ctx->has_field) ? 1 : 0;
   if (k.with_field) {
     k.nx = ctx->field.nx;
@@ -205,6 +214,23 @@ rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, in
     k.box_hi = ctx->box_hi;
     k.h = s->delta_xi;
     k.max_steps = s->max_steps;
+    k.g_nx = static_cast<unsigned>(k.nx);
+    k.g_nxny = static_cast<unsigned>(k.nx) * static_cast<unsigned>(k.ny);
+    k.g_ix = static_cast<unsigned>(k.nx - 2);
+    k.g_iy = static_cast<unsigned>(k.ny - 2);
+    k.g_iz = static_cast<unsigned>(k.nz - 2);
+    k.g_mx = static_cast<float>(k.nx - 1);
+    k.g_my = static_cast<float>(k.ny - 1);
+    k.g_mz = static_cast<float>(k.nz - 1);
+    const double h = s->delta_xi;
+    const double hs[3] = {h / k.spacing.x, h / k.spacing.y, h / k.spacing.z};
+    float* dst[6][3] = {{&k.hx, &k.hy, &k.hz},    {&k.hhx, &k.hhy, &k.hhz},
+                        {&k.kbx, &k.kby, &k.kbz}, {&k.kcx, &k.kcy, &k.kcz},
+                        {&k.krx, &k.kry, &k.krz}, {nullptr, nullptr, nullptr}};
+    const double mul[5] = {1.0, 0.5, 0.125 * h, 0.5 * h, h / 6.0};
+    for (int r = 0; r < 5; ++r)
+      for (int a = 0; a < 3; ++a) *dst[r][a] = static_cast<float>(mul[r] * hs[a]);
+    k.kt = static_cast<float>(h / 6.0);
   }
   k.n_elem = s->n_elements;
   for (int e = 0; e < s->n_elements; ++e) {

@@ -18,10 +18,11 @@
 #pragma once
 
 
+// Grid geometry, read straight from the kernel parameters (constant bank) so
+// it occupies no registers in the RK4 loop.
 struct GridView {
-  const float4* __restrict__ g;
-  unsigned nx, nxny, ix, iy, iz;  // row / plane strides, last cell index per axis
-  float mx, my, mz;               // n - 1 per axis: the box in grid coordinates
+  const KScene& S;
+  __device__ __forceinline__ explicit GridView(const KScene& s) : S(s) {}
 };
 
 // D = n grad(n) at grid coordinates (qx, qy, qz): trilinear interpolation of
@@ -29,18 +30,18 @@ struct GridView {
 // first.  Index clamp: the unsigned conversion saturates negatives to cell 0;
 // the fraction is saturated to [0, 1], which together equal clamping q.
 __device__ __forceinline__ float3 sample_d(const GridView& G, float qx, float qy, float qz) {
-  const unsigned i = min(__float2uint_rz(qx), G.ix);
-  const unsigned j = min(__float2uint_rz(qy), G.iy);
-  const unsigned k = min(__float2uint_rz(qz), G.iz);
+  const unsigned i = min(__float2uint_rz(qx), G.S.g_ix);
+  const unsigned j = min(__float2uint_rz(qy), G.S.g_iy);
+  const unsigned k = min(__float2uint_rz(qz), G.S.g_iz);
   const float fx = __saturatef(qx - (float)i);
   const float fy = __saturatef(qy - (float)j);
   const float fz = __saturatef(qz - (float)k);
-  const float4* p0 = G.g + (k * G.nxny + j * G.nx + i);
-  const float4* p1 = p0 + G.nxny;
+  const float4* p0 = G.S.grid + (k * G.S.g_nxny + j * G.S.g_nx + i);
+  const float4* p1 = p0 + G.S.g_nxny;
   const float4 c000 = __ldg(p0), c100 = __ldg(p0 + 1);
-  const float4 c010 = __ldg(p0 + G.nx), c110 = __ldg(p0 + G.nx + 1);
+  const float4 c010 = __ldg(p0 + G.S.g_nx), c110 = __ldg(p0 + G.S.g_nx + 1);
   const float4 c001 = __ldg(p1), c101 = __ldg(p1 + 1);
-  const float4 c011 = __ldg(p1 + G.nx), c111 = __ldg(p1 + G.nx + 1);
+  const float4 c011 = __ldg(p1 + G.S.g_nx), c111 = __ldg(p1 + G.S.g_nx + 1);
   const float gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
   const float w00 = gx * gy, w10 = fx * gy, w01 = gx * fy, w11 = fx * fy;
   const float w000 = w00 * gz, w100 = w10 * gz, w010 = w01 * gz, w110 = w11 * gz;
@@ -53,20 +54,144 @@ __device__ __forceinline__ float3 sample_d(const GridView& G, float qx, float qy
 #undef RB_LERP
 }
 
-__device__ __forceinline__ float sample_nm1(const GridView& G, float qx, float qy, float qz) {
-  const unsigned i = min(__float2uint_rz(qx), G.ix);
-  const unsigned j = min(__float2uint_rz(qy), G.iy);
-  const unsigned k = min(__float2uint_rz(qz), G.iz);
+// The same sample with the 8 corners of the last cell kept in registers: a step
+// advances the ray by about half a cell and its three RK stages lie within
+// that half cell, so most samples reuse the cached corners and skip the eight
+// 16-byte gathers (whose L1 -> register writeback, 384 B per ray-step, is the
+// roof of the uncached loop).
+struct CellCache {
+  unsigned key;  // linear index of the cached cell's (0,0,0) corner, ~0u = empty
+  float4 c000, c100, c010, c110, c001, c101, c011, c111;
+};
+
+__device__ __forceinline__ float3 sample_d_cached(const GridView& G, CellCache& C, float qx,
+                                                  float qy, float qz) {
+  const unsigned i = min(__float2uint_rz(qx), G.S.g_ix);
+  const unsigned j = min(__float2uint_rz(qy), G.S.g_iy);
+  const unsigned k = min(__float2uint_rz(qz), G.S.g_iz);
   const float fx = __saturatef(qx - (float)i);
   const float fy = __saturatef(qy - (float)j);
   const float fz = __saturatef(qz - (float)k);
-  const float* p0 = reinterpret_cast<const float*>(G.g + (k * G.nxny + j * G.nx + i));
-  const float* p1 = p0 + 4 * G.nxny;
+  const unsigned key = k * G.S.g_nxny + j * G.S.g_nx + i;
+  if (key != C.key) {
+    C.key = key;
+    const float4* p0 = G.S.grid + key;
+    const float4* p1 = p0 + G.S.g_nxny;
+    C.c000 = __ldg(p0);
+    C.c100 = __ldg(p0 + 1);
+    C.c010 = __ldg(p0 + G.S.g_nx);
+    C.c110 = __ldg(p0 + G.S.g_nx + 1);
+    C.c001 = __ldg(p1);
+    C.c101 = __ldg(p1 + 1);
+    C.c011 = __ldg(p1 + G.S.g_nx);
+    C.c111 = __ldg(p1 + G.S.g_nx + 1);
+  }
+  const float gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
+  const float w00 = gx * gy, w10 = fx * gy, w01 = gx * fy, w11 = fx * fy;
+  const float w000 = w00 * gz, w100 = w10 * gz, w010 = w01 * gz, w110 = w11 * gz;
+  const float w001 = w00 * fz, w101 = w10 * fz, w011 = w01 * fz, w111 = w11 * fz;
+#define RB_LERP(ch)                                                                            \
+  (w000 * C.c000.ch + w100 * C.c100.ch + w010 * C.c010.ch + w110 * C.c110.ch +                \
+   w001 * C.c001.ch + w101 * C.c101.ch + w011 * C.c011.ch + w111 * C.c111.ch)
+  const float n = 1.0f + RB_LERP(x);
+  return make_float3(RB_LERP(y) * n, RB_LERP(z) * n, RB_LERP(w) * n);
+#undef RB_LERP
+}
+
+// Cached cell in polynomial form.  On a cell change the 8 corners are loaded
+// once and turned into the coefficients of
+//   v(fx,fy,fz) = a + b fx + c fy + d fz + e fx fy + f fx fz + g fy fz + h fx fy fz
+// (the trilinear interpolant of GriddedField::sample, scene.cpp:117-133, in
+// another basis); a sample then costs 7 FFMA per channel in Horner form and
+// a 3-FADD "still in the cell" test instead of the index/weight computation.
+struct CellPoly {
+  float ox, oy, oz;  // cached cell origin (grid coordinates); ox = -1e30 = empty
+  float4 a, b, c, d, e, f, g, h;
+};
+
+__device__ __forceinline__ float4 f4sub(float4 p, float4 q) {
+  return make_float4(p.x - q.x, p.y - q.y, p.z - q.z, p.w - q.w);
+}
+
+__device__ __forceinline__ void poly_load(const GridView& G, CellPoly& P, float qx, float qy,
+                                          float qz, float& fx, float& fy, float& fz) {
+  const unsigned i = min(__float2uint_rz(qx), G.S.g_ix);
+  const unsigned j = min(__float2uint_rz(qy), G.S.g_iy);
+  const unsigned k = min(__float2uint_rz(qz), G.S.g_iz);
+  const float ox = (float)i, oy = (float)j, oz = (float)k;
+  // ClampedD: points outside the box use the face value (fraction saturated)
+  fx = __saturatef(qx - ox);
+  fy = __saturatef(qy - oy);
+  fz = __saturatef(qz - oz);
+  if (ox == P.ox && oy == P.oy && oz == P.oz) return;
+  P.ox = ox;
+  P.oy = oy;
+  P.oz = oz;
+  const float4* p0 = G.S.grid + (k * G.S.g_nxny + j * G.S.g_nx + i);
+  const float4* p1 = p0 + G.S.g_nxny;
+  const float4 c000 = __ldg(p0), c100 = __ldg(p0 + 1), c010 = __ldg(p0 + G.S.g_nx),
+               c110 = __ldg(p0 + G.S.g_nx + 1), c001 = __ldg(p1), c101 = __ldg(p1 + 1),
+               c011 = __ldg(p1 + G.S.g_nx), c111 = __ldg(p1 + G.S.g_nx + 1);
+  P.a = c000;
+  P.b = f4sub(c100, c000);
+  P.c = f4sub(c010, c000);
+  P.d = f4sub(c001, c000);
+  const float4 e0 = f4sub(c110, c010), f0 = f4sub(c101, c001), g0 = f4sub(c011, c001);
+  P.e = f4sub(e0, P.b);
+  P.f = f4sub(f0, P.b);
+  P.g = f4sub(g0, P.c);
+  P.h = f4sub(f4sub(f4sub(c111, c011), e0), P.f);  // (c111-c011) - (c110-c010) - (c101-c001) + b
+}
+
+__device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, float qx, float qy,
+                                                float qz) {
+  float fx = qx - P.ox, fy = qy - P.oy, fz = qz - P.oz;
+  // fast path: inside the cached cell (NaN fails and takes the full path)
+  const bool stay = fminf(fminf(fx, fy), fz) >= 0.0f && fmaxf(fmaxf(fx, fy), fz) <= 1.0f;
+#if RB_UNIFORM_RELOAD
+  // Warp-uniform reload: when any active lane leaves its cell, all active lanes
+  // take the reload path (lanes still inside re-derive the same cell), so the
+  // branch needs no divergence bookkeeping.
+  if (__any_sync(__activemask(), !stay)) poly_load(G, P, qx, qy, qz, fx, fy, fz);
+#else
+  if (!stay) poly_load(G, P, qx, qy, qz, fx, fy, fz);
+#endif
+#define RB_HORNER(ch)                                                                         \
+  fmaf(fx, fmaf(fz, P.f.ch, fmaf(fy, fmaf(fz, P.h.ch, P.e.ch), P.b.ch)),                     \
+       fmaf(fy, fmaf(fz, P.g.ch, P.c.ch), fmaf(fz, P.d.ch, P.a.ch)))
+  const float n = 1.0f + RB_HORNER(x);
+  return make_float3(RB_HORNER(y) * n, RB_HORNER(z) * n, RB_HORNER(w) * n);
+#undef RB_HORNER
+}
+
+#ifndef RB_UNIFORM_RELOAD
+#define RB_UNIFORM_RELOAD 1
+#endif
+#ifndef RB_CELL_CACHE
+#define RB_CELL_CACHE 2
+#endif
+#if RB_CELL_CACHE == 2
+#define RB_SAMPLE_D(qx, qy, qz) sample_d_poly(G, cache, qx, qy, qz)
+#elif RB_CELL_CACHE == 1
+#define RB_SAMPLE_D(qx, qy, qz) sample_d_cached(G, cache, qx, qy, qz)
+#else
+#define RB_SAMPLE_D(qx, qy, qz) sample_d(G, qx, qy, qz)
+#endif
+
+__device__ __forceinline__ float sample_nm1(const GridView& G, float qx, float qy, float qz) {
+  const unsigned i = min(__float2uint_rz(qx), G.S.g_ix);
+  const unsigned j = min(__float2uint_rz(qy), G.S.g_iy);
+  const unsigned k = min(__float2uint_rz(qz), G.S.g_iz);
+  const float fx = __saturatef(qx - (float)i);
+  const float fy = __saturatef(qy - (float)j);
+  const float fz = __saturatef(qz - (float)k);
+  const float* p0 = reinterpret_cast<const float*>(G.S.grid + (k * G.S.g_nxny + j * G.S.g_nx + i));
+  const float* p1 = p0 + 4 * G.S.g_nxny;
   const float gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
   return gx * gy * gz * __ldg(p0) + fx * gy * gz * __ldg(p0 + 4) +
-         gx * fy * gz * __ldg(p0 + 4 * G.nx) + fx * fy * gz * __ldg(p0 + 4 * G.nx + 4) +
+         gx * fy * gz * __ldg(p0 + 4 * G.S.g_nx) + fx * fy * gz * __ldg(p0 + 4 * G.S.g_nx + 4) +
          gx * gy * fz * __ldg(p1) + fx * gy * fz * __ldg(p1 + 4) +
-         gx * fy * fz * __ldg(p1 + 4 * G.nx) + fx * fy * fz * __ldg(p1 + 4 * G.nx + 4);
+         gx * fy * fz * __ldg(p1 + 4 * G.S.g_nx) + fx * fy * fz * __ldg(p1 + 4 * G.S.g_nx + 4);
 }
 
 __device__ __forceinline__ bool box_contains(const KScene& S, double3 p) {  // Aabb::contains
@@ -109,37 +234,27 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
   const double3 R0 = o + d * (tn + 1e-9);  // kEntryNudge, grin.cpp:85-88
   if (!box_contains(S, R0)) return kMissed;
 
-  GridView G;
-  G.g = S.grid;
-  G.nx = (unsigned)S.nx;
-  G.nxny = (unsigned)S.nx * (unsigned)S.ny;
-  G.ix = (unsigned)S.nx - 2;
-  G.iy = (unsigned)S.ny - 2;
-  G.iz = (unsigned)S.nz - 2;
-  G.mx = (float)(S.nx - 1);
-  G.my = (float)(S.ny - 1);
-  G.mz = (float)(S.nz - 1);
+  const GridView G(S);
 
   const float q0x = (float)((R0.x - S.origin.x) / S.spacing.x);
   const float q0y = (float)((R0.y - S.origin.y) / S.spacing.y);
   const float q0z = (float)((R0.z - S.origin.z) / S.spacing.z);
   const double n_e = 1.0 + (double)sample_nm1(G, q0x, q0y, q0z);
   const double3 T0 = d * n_e;  // grin.cpp:91-92
-  // Per-axis constants (grid units).  hs = h / spacing.
-  const double hsx = S.h / S.spacing.x, hsy = S.h / S.spacing.y, hsz = S.h / S.spacing.z;
-  const float ax = (float)(T0.x * hsx), ay = (float)(T0.y * hsy), az = (float)(T0.z * hsz);
-  const float hx = (float)hsx, hy = (float)hsy, hz = (float)hsz;        // dt -> dr
-  const float kbx = (float)(0.125 * S.h * hsx), kby = (float)(0.125 * S.h * hsy),
-              kbz = (float)(0.125 * S.h * hsz);                         // a/8 h
-  const float kcx = (float)(0.5 * S.h * hsx), kcy = (float)(0.5 * S.h * hsy),
-              kcz = (float)(0.5 * S.h * hsz);                           // b/2 h
-  const float krx = (float)(S.h * hsx / 6.0), kry = (float)(S.h * hsy / 6.0),
-              krz = (float)(S.h * hsz / 6.0);                           // (a+2b)/6 h
-  const float kt = (float)(S.h / 6.0);                                  // (a+4b+c)/6
-  const float hhx = 0.5f * hx, hhy = 0.5f * hy, hhz = 0.5f * hz;
+  // Per-ray advance of the unperturbed line per step, in grid units; the other
+  // RK4 constants are scene-uniform (KScene::hx ... kt).
+  const float ax = (float)(T0.x * S.h / S.spacing.x), ay = (float)(T0.y * S.h / S.spacing.y),
+              az = (float)(T0.z * S.h / S.spacing.z);
 
   float drx = 0.f, dry = 0.f, drz = 0.f, dtx = 0.f, dty = 0.f, dtz = 0.f;
   float pax = q0x, pay = q0y, paz = q0z;  // unperturbed line at xi = step * h
+#if RB_CELL_CACHE == 2
+  CellPoly cache;
+  cache.ox = cache.oy = cache.oz = -1e30f;
+#elif RB_CELL_CACHE == 1
+  CellCache cache;
+  cache.key = ~0u;
+#endif
   const int max_steps = S.max_steps;
   for (int step = 0; step < max_steps; ++step) {
     const float fs = (float)step;
@@ -147,23 +262,23 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
                 pbz = fmaf(az, fs + 0.5f, q0z);
     const float pcx = fmaf(ax, fs + 1.0f, q0x), pcy = fmaf(ay, fs + 1.0f, q0y),
                 pcz = fmaf(az, fs + 1.0f, q0z);
-    const float3 Da = sample_d(G, pax + drx, pay + dry, paz + drz);
-    const float3 Db = sample_d(G, fmaf(Da.x, kbx, fmaf(dtx, hhx, pbx + drx)),
-                               fmaf(Da.y, kby, fmaf(dty, hhy, pby + dry)),
-                               fmaf(Da.z, kbz, fmaf(dtz, hhz, pbz + drz)));
-    const float bx = fmaf(dtx, hx, drx), by = fmaf(dty, hy, dry), bz = fmaf(dtz, hz, drz);
-    const float3 Dc = sample_d(G, fmaf(Db.x, kcx, pcx + bx), fmaf(Db.y, kcy, pcy + by),
-                               fmaf(Db.z, kcz, pcz + bz));
-    const float ndrx = fmaf(fmaf(Db.x, 2.0f, Da.x), krx, bx);
-    const float ndry = fmaf(fmaf(Db.y, 2.0f, Da.y), kry, by);
-    const float ndrz = fmaf(fmaf(Db.z, 2.0f, Da.z), krz, bz);
-    const float ndtx = fmaf(fmaf(Db.x, 4.0f, Da.x) + Dc.x, kt, dtx);
-    const float ndty = fmaf(fmaf(Db.y, 4.0f, Da.y) + Dc.y, kt, dty);
-    const float ndtz = fmaf(fmaf(Db.z, 4.0f, Da.z) + Dc.z, kt, dtz);
+    const float3 Da = RB_SAMPLE_D(pax + drx, pay + dry, paz + drz);
+    const float3 Db = RB_SAMPLE_D(fmaf(Da.x, S.kbx, fmaf(dtx, S.hhx, pbx + drx)),
+                               fmaf(Da.y, S.kby, fmaf(dty, S.hhy, pby + dry)),
+                               fmaf(Da.z, S.kbz, fmaf(dtz, S.hhz, pbz + drz)));
+    const float bx = fmaf(dtx, S.hx, drx), by = fmaf(dty, S.hy, dry), bz = fmaf(dtz, S.hz, drz);
+    const float3 Dc = RB_SAMPLE_D(fmaf(Db.x, S.kcx, pcx + bx), fmaf(Db.y, S.kcy, pcy + by),
+                               fmaf(Db.z, S.kcz, pcz + bz));
+    const float ndrx = fmaf(fmaf(Db.x, 2.0f, Da.x), S.krx, bx);
+    const float ndry = fmaf(fmaf(Db.y, 2.0f, Da.y), S.kry, by);
+    const float ndrz = fmaf(fmaf(Db.z, 2.0f, Da.z), S.krz, bz);
+    const float ndtx = fmaf(fmaf(Db.x, 4.0f, Da.x) + Dc.x, S.kt, dtx);
+    const float ndty = fmaf(fmaf(Db.y, 4.0f, Da.y) + Dc.y, S.kt, dty);
+    const float ndtz = fmaf(fmaf(Db.z, 4.0f, Da.z) + Dc.z, S.kt, dtz);
     const float qx = pcx + ndrx, qy = pcy + ndry, qz = pcz + ndrz;
     // Inside the box (grid coordinates) -> accept (grin.cpp:101-106).  NaN
     // compares false, so a non-finite state always takes the exit path.
-    if (qx >= 0.0f && qx <= G.mx && qy >= 0.0f && qy <= G.my && qz >= 0.0f && qz <= G.mz) {
+    if (qx >= 0.0f && qx <= G.S.g_mx && qy >= 0.0f && qy <= G.S.g_my && qz >= 0.0f && qz <= G.S.g_mz) {
       drx = ndrx;
       dry = ndry;
       drz = ndrz;

@@ -291,8 +291,17 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
     }
     const float mass_u = 0.5f * (e - eu0);
     const float scale = energy_fx / (mass_u * mass_v);
-    float er = rb == r0 ? ev0 : erff(erf_arg(S, rb, rc));
-    for (int r = rb; r <= re; ++r) {
+    // Rows are visited starting at a lane-dependent row (wrapping once), so the
+    // lanes of a coherent warp, whose spots coincide, add to different rows at
+    // the same time instead of serialising on the same shared-memory words.
+    const int nr = re - rb + 1;
+    int r = rb + (int)(threadIdx.x & 31) % nr;
+    float er = r == r0 ? ev0 : erff(erf_arg(S, r, rc));
+    for (int jr = 0; jr < nr; ++jr, ++r) {
+      if (r > re) {
+        r = rb;
+        er = rb == r0 ? ev0 : erff(erf_arg(S, rb, rc));
+      }
       const float er1 = r == r1 ? ev1 : erff(erf_arg(S, r + 1, rc));
       const float row_w = 0.5f * (er1 - er) * scale;
       er = er1;
@@ -350,7 +359,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
   __shared__ long long sh_l[7][kBlock / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = S.rays;
-  const int K = (N + kBlock - 1) / kBlock;
+  constexpr int kWarps = kBlock / 32;
+  const int K = (S.patch_count + kWarps - 1) / kWarps;
   for (;;) {
     if (tid == 0) sh_work = atomicAdd(S.queue, 1);
     if (tid == 1) sh_box[0] = sh_box[1] = 0x7fffffff;
@@ -365,17 +375,23 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
 
     double su = 0.0, sv = 0.0;
     long long cnt[7] = {0, 0, 0, 0, 0, 0, 0};  // landed, lost, aperture, miss, tir, smiss, steps
-    const int i_begin = tid * K, i_end = min(i_begin + K, N);
 
     // One loop, one trace_ray call site: iteration 0 is the pilot, after which
     // the CTA places the tile.  __syncwarp() reconverges the lanes after every
     // ray so a warp never splits into groups running different rays' RK4 loops.
     int tc0 = 0, tr0 = 0, tw = 0, th = 0;
     for (int k = 0; k < K; ++k) {
-      const int i = i_begin + k;
+      int i = -1;
+      const int slot = k * kWarps + warp;
+      if (slot < S.patch_count) {
+        const int p = (int)(((long long)slot * S.patch_stride) % S.patch_count);
+        const int py = p / S.patch_px, px = p - py * S.patch_px;
+        const int cx = px * 8 + (lane & 7), cy = py * 4 + (lane >> 3);
+        if (cx < S.cells && cy * S.cells + cx < N) i = cy * S.cells + cx;
+      }
       RayResult r;
       r.status = -1;
-      if (i < i_end) r = trace_ray(S, ekey, so, i);
+      if (i >= 0) r = trace_ray(S, ekey, so, i);
       if (k == 0 && S.accumulate) {  // block-uniform branch
         if (r.status == 0) {  // spot_pixel_window of the pilot, clipped to the frame
           const double cc = r.u / S.pitch + 0.5 * S.W;

@@ -13,7 +13,7 @@ constexpr int kMaxElements = 8;
 #define RB_BLOCK 256
 #endif
 #ifndef RB_MINB
-#define RB_MINB 3
+#define RB_MINB 2
 #endif
 constexpr int kBlock = RB_BLOCK;     // threads per CTA (one emitter at a time)
 constexpr int kMinBlocks = RB_MINB;  // resident CTAs per SM the register budget targets
@@ -54,11 +54,30 @@ struct KScene {
   int32_t cells;                 // ceil(sqrt(N))
   int32_t sampling;
   int32_t with_field;
+  // warp patches: each warp-iteration traces a compact 8x4 block of the pupil
+  // lattice (cells x rows, ray i = cy * cells + cx) so its 32 rays gather from
+  // the same few grid cells; patches are visited in a strided order so the
+  // first iteration (the tile pilot) samples the whole pupil.
+  int32_t patch_px;              // patches per lattice row (ceil(cells / 8))
+  int32_t patch_count;
+  int32_t patch_stride;          // coprime to patch_count
+  int32_t pad_patch;
   // density grid (float4: n-1, dn/dx, dn/dy, dn/dz)
   const float4* grid;
   int32_t nx, ny, nz, max_steps;
   double3 origin, spacing, box_lo, box_hi;
   double h;
+  // scene-uniform GRIN constants (host-computed; read as constant-bank operands
+  // so they take no registers in the RK4 loop)
+  unsigned g_nx, g_nxny, g_ix, g_iy, g_iz;  // strides, last cell index per axis
+  float g_mx, g_my, g_mz;                   // n - 1 per axis (box in grid coordinates)
+  float hx, hy, hz;                         // h / spacing          (dt -> dr)
+  float hhx, hhy, hhz;                      // h / spacing / 2
+  float kbx, kby, kbz;                      // h^2 / spacing / 8    (a/8 h)
+  float kcx, kcy, kcz;                      // h^2 / spacing / 2    (b/2 h)
+  float krx, kry, krz;                      // h^2 / spacing / 6    ((a+2b)/6 h)
+  float kt;                                 // h / 6                ((a+4b+c)/6)
+  float pad_g;
   // optics (optics.cpp:143-158)
   int32_t n_elem, pad1;
   DElement elem[kMaxElements];
