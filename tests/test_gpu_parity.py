@@ -158,3 +158,21 @@ def test_no_accumulate_leaves_stats_only(tracer):
     res = tracer.run_trace(scene, True, accumulate_image=False)
     assert res.image is None
     assert np.array_equal(res.landed, g["landed_1"])
+
+
+def test_cpp_dropin_adapter_matches_reference():
+    """include/raybos_gpu/run_trace.hpp — the C++ drop-in with the reference's exact
+    signature — driven on the reference's own SceneSetups and bos_run metric chain
+    (oracle/adapter_parity.cpp, prebuilt against the reference headers)."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle",
+                       "_ref", "adapter_parity")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/adapter_parity not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    bad = [l for l in lines if l.get("ok") is False]
+    assert r.returncode == 0 and not bad, (bad, r.stderr[-2000:])
+    assert sum(1 for l in lines if "check" in l) >= 9
