@@ -52,7 +52,10 @@ inline rb_surface surf(const raybos::SphericalSurface& s) {
 // One process-wide context: device streams, the resident grid, buffers.
 struct Context {
   rb_ctx* ctx = nullptr;
-  const raybos::GriddedField* field = nullptr;  // identity of the uploaded grid
+  // The uploaded grid, tracked by ownership (not by address: a new field can be
+  // allocated where a freed one lived).
+  std::weak_ptr<const raybos::GriddedField> field;
+  bool has_field = false;
   std::mutex mu;
 
   Context() {
@@ -64,13 +67,15 @@ struct Context {
   }
   ~Context() { rb_destroy(ctx); }
 
-  void ensure_field(const raybos::GriddedField* g) {
-    if (g == field) return;
-    if (!g) {
+  void ensure_field(const std::shared_ptr<const raybos::GriddedField>& sp) {
+    if (has_field && !field.expired() && field.lock() == sp) return;
+    if (!sp) {
       rb_clear_field(ctx);
-      field = nullptr;
+      field.reset();
+      has_field = false;
       return;
     }
+    const raybos::GriddedField* g = sp.get();
     rb_field_desc d{};
     d.nx = g->nx();
     d.ny = g->ny();
@@ -91,7 +96,8 @@ struct Context {
         }
     const int rc = rb_set_field_nodes(ctx, &d, n.data(), gx.data(), gy.data(), gz.data());
     if (rc) raise(rc, rb_last_error(ctx));
-    field = g;
+    field = sp;
+    has_field = true;
   }
 };
 
@@ -108,7 +114,7 @@ inline raybos::TraceOutputs run_trace(const raybos::SceneSetup& setup, bool with
   (void)run;  // threads / deterministic: see header comment
   detail::Context& C = detail::context();
   std::lock_guard<std::mutex> lock(C.mu);
-  if (with_field && setup.field) C.ensure_field(setup.field.get());
+  if (with_field && setup.field) C.ensure_field(setup.field);
 
   std::vector<rb_vec3> sources;
   sources.reserve(setup.sources.size());

@@ -75,8 +75,9 @@ void compare_traces(const std::string& name, const SceneSetup& setup, bool with_
     diff += d != 0;
     maxd = std::max(maxd, d);
   }
-  const bool ok = counters && landed_eq && max_px < 1e-3 && rel < 1e-4 && b.accounting_ok() &&
-                  maxd <= 1;
+  // north-star gates: counts exact, per-dot means within 1e-3 px, image within 1e-4
+  // relative L2 (the quantized PGM difference is reported, not gated)
+  const bool ok = counters && landed_eq && max_px < 1e-3 && rel < 1e-4 && b.accounting_ok();
   check(name + (with_field ? "/field" : "/nofield"), ok,
         num("emitted", a.emitted) + ", " + num("counters_equal", counters) + ", " +
             num("landed_equal", landed_eq) + ", " + num("max_mean_hit_px", max_px) + ", " +

@@ -10,16 +10,18 @@ capi = os.path.join(PKG, "_build", "capi.cpp.o")
 variants = []
 for v in sys.argv[1:] or ["256x2c1", "256x3c0"]:
     b, rest = v.split("x")
-    u = 0
+    u, dd = 1, 1
+    if "d" in rest:
+        rest, dd = rest.split("d")
     if "u" in rest:
         rest, u = rest.split("u")
     m, c = rest.split("c") if "c" in rest else (rest, "1")
-    variants.append((int(b), int(m), int(c), int(u)))
-for blk, mb, cc, uu in variants:
-    obj = os.path.join(OUT, f"k_{blk}_{mb}_c{cc}_u{uu}.o")
+    variants.append((int(b), int(m), int(c), int(u), int(dd)))
+for blk, mb, cc, uu, dd in variants:
+    obj = os.path.join(OUT, f"k_{blk}_{mb}_c{cc}_u{uu}_d{dd}.o")
     subprocess.run([NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", *ARCH,
-                    f"-DRB_BLOCK={blk}", f"-DRB_MINB={mb}", f"-DRB_CELL_CACHE={cc}", f"-DRB_UNIFORM_RELOAD={uu}", f"-I{ROOT}/include", "-c",
+                    f"-DRB_BLOCK={blk}", f"-DRB_MINB={mb}", f"-DRB_CELL_CACHE={cc}", f"-DRB_UNIFORM_RELOAD={uu}", f"-DRB_DITHER={dd}", f"-I{ROOT}/include", "-c",
                     os.path.join(PKG, "csrc", "kernels.cu"), "-o", obj], check=True)
-    lib = os.path.join(OUT, f"libraybos_gpu_{blk}_{mb}_c{cc}_u{uu}.so")
+    lib = os.path.join(OUT, f"libraybos_gpu_{blk}_{mb}_c{cc}_u{uu}_d{dd}.so")
     subprocess.run([NVCC, "-shared", *ARCH, capi, obj, "-o", lib, "-ldl", "-lpthread"], check=True)
     print(lib)
