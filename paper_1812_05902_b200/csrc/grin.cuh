@@ -226,7 +226,10 @@ __device__ __forceinline__ bool aabb_intersect(const KScene& S, double3 o, doubl
 }
 
 // Returns kMissed / kTraced / kLost / kInvalid; on kTraced (o, d) is the exit ray.
-__device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& d, int& steps) {
+// scratch: 7 doubles of shared memory for this thread; R0 and T0 are parked
+// there during the RK4 loop (they are only needed again at the exit).
+__device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& d, int& steps,
+                                          double* scratch) {
   steps = 0;
   double tn;
   if (!aabb_intersect(S, o, d, tn)) return kMissed;
@@ -245,6 +248,13 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
   // RK4 constants are scene-uniform (KScene::hx ... kt).
   const float ax = (float)(T0.x * S.h / S.spacing.x), ay = (float)(T0.y * S.h / S.spacing.y),
               az = (float)(T0.z * S.h / S.spacing.z);
+  // park the FP64 entry state; it is read back only at the exit
+  scratch[0] = R0.x;
+  scratch[1] = R0.y;
+  scratch[2] = R0.z;
+  scratch[3] = T0.x;
+  scratch[4] = T0.y;
+  scratch[5] = T0.z;
 
   float drx = 0.f, dry = 0.f, drz = 0.f, dtx = 0.f, dty = 0.f, dtz = 0.f;
   float pax = q0x, pay = q0y, paz = q0z;  // unperturbed line at xi = step * h
@@ -297,6 +307,9 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
     }
     // Crossed the boundary: cut back to the first face crossing (grin.cpp:110-130),
     // evaluated on the FP64 reconstruction of both states.
+    const volatile double* vs = scratch;
+    const double3 R0 = make_double3(vs[0], vs[1], vs[2]);
+    const double3 T0 = make_double3(vs[3], vs[4], vs[5]);
     const double xi0 = (double)step * S.h, xi1 = (double)(step + 1) * S.h;
     const double3 r0 = make_double3(R0.x + T0.x * xi0 + (double)drx * S.spacing.x,
                                     R0.y + T0.y * xi0 + (double)dry * S.spacing.y,

@@ -209,7 +209,8 @@ struct RayResult {
 };
 
 // process_source's per-ray body, engine.cpp:112-137.
-__device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, double3 src, int i) {
+__device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, double3 src, int i,
+                                               double* scratch) {
   RayResult r;
   r.steps = 0;
   r.u = r.v = 0.0;
@@ -223,7 +224,7 @@ __device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, d
   }
   double3 o = src, d = to / len;
   if (S.with_field) {
-    const int st = grin_trace(S, o, d, r.steps);
+    const int st = grin_trace(S, o, d, r.steps, scratch);
     if (st == kLost || st == kInvalid) {
       r.status = 1;  // RB_RAY_LOST
       return r;
@@ -368,33 +369,52 @@ __device__ __forceinline__ T warp_sum(T v) {
 // whole pupil lattice).  Deposits outside the tile go straight to global.
 __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __grid_constant__ KScene S) {
   extern __shared__ uint32_t tile[];
-  __shared__ int sh_work;
+  constexpr int kWarps = kBlock / 32;
+  __shared__ int sh_work, sh_src;
   __shared__ int sh_box[4];
-  __shared__ double sh_d[2][kBlock / 32];
-  __shared__ long long sh_l[7][kBlock / 32];
+  __shared__ int sh_tile[4];                 // tc0, tr0, tw, th
+  __shared__ double sh_so[3];                // emitter position
+  __shared__ unsigned long long sh_ekey;     // per-emitter RNG key
+  // Per-thread emitter accumulators and the GRIN entry state live in shared
+  // memory, not registers: they change once per ray, and keeping them out of
+  // the register file during the RK4 loop is what lets K1 fit its budget.
+  __shared__ double sh_uv[2][kBlock];
+  __shared__ unsigned sh_cnt[7][kBlock];     // landed, lost, aperture, miss, tir, smiss, steps
+  __shared__ double sh_rt[kBlock][7];        // R0, T0 of the ray in flight (grin.cuh)
+  __shared__ double sh_d[2][kWarps];
+  __shared__ unsigned long long sh_l[7][kWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = S.rays;
-  constexpr int kWarps = kBlock / 32;
   const int K = (S.patch_count + kWarps - 1) / kWarps;
+  volatile double* vso = sh_so;
+  volatile unsigned long long* vkey = &sh_ekey;
+  volatile int* vtile = sh_tile;
   for (;;) {
-    if (tid == 0) sh_work = atomicAdd(S.queue, 1);
-    if (tid == 1) sh_box[0] = sh_box[1] = 0x7fffffff;
-    if (tid == 2) sh_box[2] = sh_box[3] = -1;
+    if (tid == 0) {
+      const int w = atomicAdd(S.queue, 1);
+      sh_work = w;
+      if (w < S.n_work) {
+        const int src = S.order[w];
+        sh_src = src;
+        const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
+        sh_ekey = mix_bits(S.key_seed + sid);
+        sh_so[0] = S.sources[3 * src];
+        sh_so[1] = S.sources[3 * src + 1];
+        sh_so[2] = S.sources[3 * src + 2];
+      }
+      sh_box[0] = sh_box[1] = 0x7fffffff;
+      sh_box[2] = sh_box[3] = -1;
+      sh_tile[0] = sh_tile[1] = sh_tile[2] = sh_tile[3] = 0;
+    }
+    sh_uv[0][tid] = sh_uv[1][tid] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 7; ++j) sh_cnt[j][tid] = 0u;
     __syncthreads();
-    const int w = sh_work;
-    if (w >= S.n_work) break;
-    const int src = S.order[w];
-    const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
-    const double3 so = make_double3(S.sources[3 * src], S.sources[3 * src + 1], S.sources[3 * src + 2]);
-    const uint64_t ekey = mix_bits(S.key_seed + sid);
-
-    double su = 0.0, sv = 0.0;
-    long long cnt[7] = {0, 0, 0, 0, 0, 0, 0};  // landed, lost, aperture, miss, tir, smiss, steps
+    if (sh_work >= S.n_work) break;
 
     // One loop, one trace_ray call site: iteration 0 is the pilot, after which
     // the CTA places the tile.  __syncwarp() reconverges the lanes after every
     // ray so a warp never splits into groups running different rays' RK4 loops.
-    int tc0 = 0, tr0 = 0, tw = 0, th = 0;
     for (int k = 0; k < K; ++k) {
       int i = -1;
       const int slot = k * kWarps + warp;
@@ -404,9 +424,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
         const int cx = px * 8 + (lane & 7), cy = py * 4 + (lane >> 3);
         if (cx < S.cells && cy * S.cells + cx < N) i = cy * S.cells + cx;
       }
+      const uint64_t ekey = *vkey;
       RayResult r;
       r.status = -1;
-      if (i >= 0) r = trace_ray(S, ekey, so, i);
+      if (i >= 0) r = trace_ray(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid]);
       if (k == 0 && S.accumulate) {  // block-uniform branch
         if (r.status == 0) {  // spot_pixel_window of the pilot, clipped to the frame
           const double cc = r.u / S.pitch + 0.5 * S.W;
@@ -423,51 +444,54 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
           }
         }
         __syncthreads();
-        if (sh_box[2] >= 0) {
+        if (tid == 0 && sh_box[2] >= 0) {
           const int m = 2;
           const int bw = sh_box[2] - sh_box[0] + 1 + 2 * m, bh = sh_box[3] - sh_box[1] + 1 + 2 * m;
-          tw = min(bw, S.W);
-          th = min(bh, S.H);
+          int tw = min(bw, S.W), th = min(bh, S.H);
           if (tw * th > kTileCap) {
             const float f = sqrtf((float)kTileCap / (float)(tw * th));
             tw = max(1, min(tw, (int)(tw * f)));
             th = max(1, min(th, kTileCap / tw));
           }
           const int ccen = (sh_box[0] + sh_box[2]) / 2, rcen = (sh_box[1] + sh_box[3]) / 2;
-          tc0 = min(max(ccen - tw / 2, 0), S.W - tw);
-          tr0 = min(max(rcen - th / 2, 0), S.H - th);
+          sh_tile[0] = min(max(ccen - tw / 2, 0), S.W - tw);
+          sh_tile[1] = min(max(rcen - th / 2, 0), S.H - th);
+          sh_tile[2] = tw;
+          sh_tile[3] = th;
         }
-        for (int q = tid; q < tw * th; q += kBlock) tile[q] = 0u;
+        __syncthreads();
+        for (int q = tid; q < sh_tile[2] * sh_tile[3]; q += kBlock) tile[q] = 0u;
         __syncthreads();
       }
       if (r.status >= 0) {
-        cnt[6] += r.steps;
-#pragma unroll
-        for (int j = 0; j < 6; ++j) cnt[j] += (r.status == j);
+        sh_cnt[6][tid] += (unsigned)r.steps;
+        sh_cnt[r.status][tid] += 1u;
         if (r.status == 0) {
-          su += r.u;
-          sv += r.v;
+          sh_uv[0][tid] += r.u;
+          sh_uv[1][tid] += r.v;
           if (S.accumulate)
-            deposit(S, r.u, r.v, tile, tc0, tr0, tw, th,
+            deposit(S, r.u, r.v, tile, vtile[0], vtile[1], vtile[2], vtile[3],
                     (uint32_t)(mix_bits(ekey + (uint64_t)i) >> 32));
         }
       }
       __syncwarp();
     }
 
-    // per-emitter stats: DotHitStats (bos.hpp:71-74) + counters
-    su = warp_sum(su);
-    sv = warp_sum(sv);
+    // per-emitter stats: DotHitStats (bos.hpp:71-74) + counters, fixed order
+    double su = warp_sum(sh_uv[0][tid]);
+    double sv = warp_sum(sh_uv[1][tid]);
+    unsigned long long cnt[7];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) cnt[k] = warp_sum(cnt[k]);
+    for (int j = 0; j < 7; ++j) cnt[j] = warp_sum((unsigned long long)sh_cnt[j][tid]);
     if (lane == 0) {
       sh_d[0][warp] = su;
       sh_d[1][warp] = sv;
 #pragma unroll
-      for (int k = 0; k < 7; ++k) sh_l[k][warp] = cnt[k];
+      for (int j = 0; j < 7; ++j) sh_l[j][warp] = cnt[j];
     }
     __syncthreads();
     if (S.accumulate) {  // flush the tile (composite_tile, engine.cpp:181-187)
+      const int tc0 = sh_tile[0], tr0 = sh_tile[1], tw = sh_tile[2], th = sh_tile[3];
       for (int q = tid; q < tw * th; q += kBlock) {
         const uint32_t f = tile[q];
         if (f) {
@@ -478,19 +502,20 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
     }
     if (tid == 0) {
       double a = 0.0, b = 0.0;
-      long long l[7] = {0, 0, 0, 0, 0, 0, 0};
-      for (int k = 0; k < kBlock / 32; ++k) {
+      unsigned long long l[7] = {0, 0, 0, 0, 0, 0, 0};
+      for (int k = 0; k < kWarps; ++k) {
         a += sh_d[0][k];
         b += sh_d[1][k];
 #pragma unroll
         for (int j = 0; j < 7; ++j) l[j] += sh_l[j][k];
       }
+      const int src = sh_src;
       S.hit_sum[2 * src] = a;
       S.hit_sum[2 * src + 1] = b;
-      S.landed[src] = l[0];
+      S.landed[src] = (long long)l[0];
 #pragma unroll
       for (int j = 1; j < 7; ++j)
-        if (l[j]) atomicAdd(&S.counters[j - 1], (unsigned long long)l[j]);
+        if (l[j]) atomicAdd(&S.counters[j - 1], l[j]);
     }
     __syncthreads();
   }
@@ -500,12 +525,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
 __global__ void trace_rays_kernel(const __grid_constant__ KScene S, int64_t n,
                                   const int64_t* __restrict__ srcs, const int32_t* __restrict__ rays,
                                   double* uv, int32_t* status, int32_t* steps) {
+  __shared__ double sh_rt[128][7];
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const int64_t src = srcs[q];
   const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
   const double3 so = make_double3(S.sources[3 * src], S.sources[3 * src + 1], S.sources[3 * src + 2]);
-  const RayResult r = trace_ray(S, mix_bits(S.key_seed + sid), so, rays[q]);
+  const RayResult r = trace_ray(S, mix_bits(S.key_seed + sid), so, rays[q], sh_rt[threadIdx.x]);
   uv[2 * q] = r.status == 0 ? r.u : nan("");
   uv[2 * q + 1] = r.status == 0 ? r.v : nan("");
   status[q] = r.status;

@@ -1,0 +1,17 @@
+"""Reports spill instructions inside K1's GRIN loop for a cubin/.so (dev aid)."""
+import re, subprocess, sys
+sass = subprocess.run(["cuobjdump", "-sass", sys.argv[1]], capture_output=True, text=True).stdout
+body = sass[sass.index("Function : _ZN3rbk15render_emitters"):]
+body = body[:body.index("Function :", 20)] if "Function :" in body[20:] else body
+lines = [l for l in body.splitlines() if re.match(r'\s+/\*[0-9a-f]{4,5}\*/', l)]
+addr = [int(re.match(r'\s+/\*([0-9a-f]+)\*/', l).group(1), 16) for l in lines]
+for i, l in enumerate(lines):
+    m = re.search(r'BRA\s+(?:`\()?0x([0-9a-f]+)', l)
+    if m and int(m.group(1), 16) < addr[i]:
+        t = int(m.group(1), 16)
+        region = [x for x, a in zip(lines, addr) if t <= a <= addr[i]]
+        if any('LDG.E.128' in x for x in region) and len(region) < 1200:
+            sp = [x for x in region if 'STL' in x or 'LDL' in x]
+            print(f"GRIN loop {hex(t)}-{hex(addr[i])}: {len(region)} instr, {len(sp)} spill instr")
+            break
+print("total spill instr", sum(1 for x in lines if 'STL' in x or 'LDL' in x))
