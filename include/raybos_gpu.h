@@ -232,6 +232,23 @@ int rb_trace_rays(rb_ctx* ctx, const rb_scene* scene, int with_field, int64_t n_
                   const int64_t* source_index, const int32_t* ray_index, double* uv,
                   int32_t* status, int32_t* steps);
 
+/* ---- FP64 validation build ------------------------------------------------ */
+/* The per-ray pipeline in FP64 with the reference's operation order and no FMA
+ * contraction: GRIN samples the FP64 GriddedField nodes exactly like
+ * GriddedField::sample (scene.cpp:99-135) and integrates trace_through_volume
+ * (grin.cpp:74-134) literally.  Results are bit-identical to the reference
+ * except where the device sin/cos in concentric_disk_map (raygen.cpp:24) differ
+ * from glibc's by an ulp.  Needs the FP64 node copy the context keeps for grids
+ * of at most RB_FP64_MAX_NODES nodes.  Validation only (one thread per ray). */
+#define RB_FP64_MAX_NODES (1LL << 26)
+int rb_trace_rays_fp64(rb_ctx* ctx, const rb_scene* scene, int with_field, int64_t n_rays,
+                       const int64_t* source_index, const int32_t* ray_index, double* uv,
+                       int32_t* status, int32_t* steps);
+/* Per-source DotHitStats and counters of the FP64 validation build, rays summed
+ * in the reference's order (engine.cpp:112-137): hit_sum / landed / counters
+ * bit-identical to the reference under the same sin/cos caveat.  No image. */
+int rb_trace_stats_fp64(rb_ctx* ctx, const rb_scene* scene, int with_field, rb_trace_out* out);
+
 #ifdef __cplusplus
 }
 #endif

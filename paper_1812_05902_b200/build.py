@@ -54,6 +54,8 @@ def build_library(verbose: bool = False, force: bool = False) -> str:
                  f"-I{os.path.join(ROOT, 'include')}"]
         if src.endswith(".cu"):
             flags += ARCH + ["-Xptxas", "-v"]
+            if src == "kernels_fp64.cu":      # FP64 validation build: no FMA contraction
+                flags += ["-fmad=false"]
         else:
             flags += ["-x", "c++", "-Wno-deprecated-gpu-targets"]
         out = _run([NVCC] + flags + ["-c", path, "-o", obj], verbose)

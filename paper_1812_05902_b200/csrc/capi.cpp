@@ -63,6 +63,7 @@ struct Device {
   size_t grid_bytes = 0;
   Buf sources, ids, order, image, hit, landed, counters, queue, err, dimage, rays_src, rays_idx,
       rays_uv, rays_status, rays_steps;
+  Buf f64[4];  // FP64 node copy (n, gx, gy, gz) for the validation build
 };
 
 struct NcclApi {
@@ -98,6 +99,7 @@ struct rb_ctx {
   std::vector<Device> devs;
   std::string last_error;
   bool has_field = false;
+  bool has_field64 = false;  // FP64 node copy present (grids <= RB_FP64_MAX_NODES)
   rb_field_desc field{};
   double3 box_lo{}, box_hi{};
   NcclApi nccl;
@@ -451,6 +453,7 @@ void set_box(rb_ctx* ctx, const rb_field_desc* d) {
                              d->origin.y + (d->ny - 1) * d->spacing.y,
                              d->origin.z + (d->nz - 1) * d->spacing.z);
   ctx->has_field = true;
+  ctx->has_field64 = static_cast<long long>(d->nx) * d->ny * d->nz <= RB_FP64_MAX_NODES;
 }
 
 }  // namespace
@@ -527,6 +530,7 @@ void rb_destroy(rb_ctx* ctx) {
   for (Device& d : ctx->devs) {
     cudaSetDevice(d.ordinal);
     if (d.grid) cudaFree(d.grid);
+    for (Buf& b : d.f64) b.release();
     for (Buf* b : {&d.sources, &d.ids, &d.order, &d.image, &d.hit, &d.landed, &d.counters,
                    &d.queue, &d.err, &d.dimage, &d.rays_src, &d.rays_idx, &d.rays_uv,
                    &d.rays_status, &d.rays_steps})
@@ -559,6 +563,15 @@ int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, 
       RB_CUDA(ctx, rbk::launch_pack_nodes(st, st + chunk, st + 2 * chunk, st + 3 * chunk,
                                           dev.grid + off, static_cast<int64_t>(m), dev.stream));
     }
+    for (Buf& b : dev.f64) b.release();
+    if (static_cast<long long>(count) <= RB_FP64_MAX_NODES) {
+      const double* src[4] = {n, gx, gy, gz};
+      for (int a = 0; a < 4; ++a) {
+        RB_CUDA(ctx, dev.f64[a].ensure(count * sizeof(double)));
+        RB_CUDA(ctx, cudaMemcpyAsync(dev.f64[a].p, src[a], count * sizeof(double),
+                                     cudaMemcpyHostToDevice, dev.stream));
+      }
+    }
     RB_CUDA(ctx, cudaStreamSynchronize(dev.stream));
     stage.release();
     set_l2_window(dev);
@@ -587,6 +600,14 @@ int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rh
     RB_CUDA(ctx, rbk::launch_build_from_density(drho.as<float>(), desc->nx, desc->ny, desc->nz,
                                                 gladstone_dale_k, d3(desc->spacing), dev.grid, 0,
                                                 desc->nz, dev.stream));
+    for (Buf& b : dev.f64) b.release();
+    if (static_cast<long long>(count) <= RB_FP64_MAX_NODES) {
+      for (Buf& b : dev.f64) RB_CUDA(ctx, b.ensure(count * sizeof(double)));
+      RB_CUDA(ctx, rbk::launch_build_fp64(drho.as<float>(), desc->nx, desc->ny, desc->nz,
+                                          gladstone_dale_k, d3(desc->spacing), dev.f64[0].as<double>(),
+                                          dev.f64[1].as<double>(), dev.f64[2].as<double>(),
+                                          dev.f64[3].as<double>(), dev.stream));
+    }
     RB_CUDA(ctx, cudaStreamSynchronize(dev.stream));
     drho.release();
     set_l2_window(dev);
@@ -603,7 +624,12 @@ int rb_clear_field(rb_ctx* ctx) {
     dev.grid = nullptr;
     dev.grid_bytes = 0;
   }
+  for (Device& dev : ctx->devs) {
+    cudaSetDevice(dev.ordinal);
+    for (Buf& b : dev.f64) b.release();
+  }
   ctx->has_field = false;
+  ctx->has_field64 = false;
   return RB_OK;
 }
 
@@ -823,3 +849,146 @@ int rb_trace_rays(rb_ctx* ctx, const rb_scene* s, int with_field, int64_t n_rays
 }
 
 }  // extern "C"
+
+
+// ---- FP64 validation build ------------------------------------------------
+namespace {
+
+int upload_scene_arrays(rb_ctx* ctx, Device& dev, const rb_scene* s, rbk::KScene& k) {
+  const int64_t n = s->n_sources;
+  RB_CUDA(ctx, dev.sources.ensure(sizeof(double) * 3 * std::max<int64_t>(n, 1)));
+  if (n)
+    RB_CUDA(ctx, cudaMemcpyAsync(dev.sources.p, s->sources, sizeof(double) * 3 * n,
+                                 cudaMemcpyHostToDevice, dev.stream));
+  k.sources = dev.sources.as<double>();
+  k.source_ids = nullptr;
+  if (s->source_ids && n) {
+    RB_CUDA(ctx, dev.ids.ensure(sizeof(int64_t) * n));
+    RB_CUDA(ctx, cudaMemcpyAsync(dev.ids.p, s->source_ids, sizeof(int64_t) * n,
+                                 cudaMemcpyHostToDevice, dev.stream));
+    k.source_ids = dev.ids.as<int64_t>();
+  }
+  RB_CUDA(ctx, dev.queue.ensure(sizeof(int) * 2));
+  RB_CUDA(ctx, cudaMemsetAsync(dev.queue.p, 0, sizeof(int) * 2, dev.stream));
+  k.err_flag = dev.queue.as<int>() + 1;
+  return RB_OK;
+}
+
+int field64(rb_ctx* ctx, const Device& dev, int with_field, rbk::Field64& f) {
+  f = rbk::Field64{};
+  if (!(with_field && ctx->has_field)) return RB_OK;
+  if (!ctx->has_field64 || !dev.f64[0].p)
+    return fail(ctx, RB_E_INVALID, "rb_*_fp64: the FP64 validation build needs a grid of at most "
+                                   "2^26 nodes");
+  f.n = dev.f64[0].as<double>();
+  f.gx = dev.f64[1].as<double>();
+  f.gy = dev.f64[2].as<double>();
+  f.gz = dev.f64[3].as<double>();
+  f.nx = ctx->field.nx;
+  f.ny = ctx->field.ny;
+  f.nz = ctx->field.nz;
+  f.origin = d3(ctx->field.origin);
+  f.spacing = d3(ctx->field.spacing);
+  f.lo = ctx->box_lo;
+  f.hi = ctx->box_hi;
+  return RB_OK;
+}
+
+}  // namespace
+
+extern "C" int rb_trace_rays_fp64(rb_ctx* ctx, const rb_scene* s, int with_field, int64_t n_rays,
+                                  const int64_t* source_index, const int32_t* ray_index,
+                                  double* uv, int32_t* status, int32_t* steps) {
+  if (!ctx) return RB_E_INVALID;
+  if (int rc = validate_scene(ctx, s)) return rc;
+  if (n_rays <= 0) return RB_OK;
+  for (int64_t q = 0; q < n_rays; ++q)
+    if (source_index[q] < 0 || source_index[q] >= s->n_sources || ray_index[q] < 0 ||
+        ray_index[q] >= s->rays_per_source)
+      return fail(ctx, RB_E_INVALID, "rb_trace_rays_fp64: (source, ray) index out of range");
+  Device& dev = ctx->devs[0];
+  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+  rbk::KScene k = make_kscene(ctx, s, with_field, 0);
+  rbk::Field64 f;
+  if (int rc = field64(ctx, dev, with_field, f)) return rc;
+  if (int rc = upload_scene_arrays(ctx, dev, s, k)) return rc;
+  cudaStream_t st = dev.stream;
+  RB_CUDA(ctx, dev.rays_src.ensure(sizeof(int64_t) * n_rays));
+  RB_CUDA(ctx, dev.rays_idx.ensure(sizeof(int32_t) * n_rays));
+  RB_CUDA(ctx, dev.rays_uv.ensure(sizeof(double) * 2 * n_rays));
+  RB_CUDA(ctx, dev.rays_status.ensure(sizeof(int32_t) * n_rays));
+  RB_CUDA(ctx, dev.rays_steps.ensure(sizeof(int32_t) * n_rays));
+  RB_CUDA(ctx, cudaMemcpyAsync(dev.rays_src.p, source_index, sizeof(int64_t) * n_rays,
+                               cudaMemcpyHostToDevice, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(dev.rays_idx.p, ray_index, sizeof(int32_t) * n_rays,
+                               cudaMemcpyHostToDevice, st));
+  RB_CUDA(ctx, rbk::launch_trace_rays_fp64(k, f, n_rays, dev.rays_src.as<int64_t>(),
+                                           dev.rays_idx.as<int32_t>(), dev.rays_uv.as<double>(),
+                                           dev.rays_status.as<int32_t>(),
+                                           dev.rays_steps.as<int32_t>(), st));
+  RB_CUDA(ctx, cudaMemcpyAsync(uv, dev.rays_uv.p, sizeof(double) * 2 * n_rays,
+                               cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(status, dev.rays_status.p, sizeof(int32_t) * n_rays,
+                               cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(steps, dev.rays_steps.p, sizeof(int32_t) * n_rays,
+                               cudaMemcpyDeviceToHost, st));
+  int flag = 0;
+  RB_CUDA(ctx, cudaMemcpyAsync(&flag, k.err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaStreamSynchronize(st));
+  if (flag) return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+  return RB_OK;
+}
+
+extern "C" int rb_trace_stats_fp64(rb_ctx* ctx, const rb_scene* s, int with_field,
+                                   rb_trace_out* out) {
+  if (!ctx || !out) return RB_E_INVALID;
+  const auto t0 = std::chrono::steady_clock::now();
+  if (int rc = validate_scene(ctx, s)) return rc;
+  const unsigned long long zero[6] = {0, 0, 0, 0, 0, 0};
+  out->threads = 1;
+  out->kernel_ms = 0.0;
+  if (s->n_sources == 0) {
+    fill_report(out, s, 0, zero, 0);
+    return RB_OK;
+  }
+  Device& dev = ctx->devs[0];
+  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+  rbk::KScene k = make_kscene(ctx, s, with_field, 0);
+  rbk::Field64 f;
+  if (int rc = field64(ctx, dev, with_field, f)) return rc;
+  if (int rc = upload_scene_arrays(ctx, dev, s, k)) return rc;
+  const int64_t n = s->n_sources;
+  cudaStream_t st = dev.stream;
+  RB_CUDA(ctx, dev.hit.ensure(sizeof(double) * 2 * n));
+  RB_CUDA(ctx, dev.landed.ensure(sizeof(long long) * n));
+  RB_CUDA(ctx, dev.counters.ensure(sizeof(unsigned long long) * 8));
+  RB_CUDA(ctx, cudaMemsetAsync(dev.counters.p, 0, sizeof(unsigned long long) * 8, st));
+  k.hit_sum = dev.hit.as<double>();
+  k.landed = dev.landed.as<long long>();
+  k.counters = dev.counters.as<unsigned long long>();
+  RB_CUDA(ctx, rbk::launch_source_stats_fp64(k, f, st));
+  std::vector<double> hit(2 * n);
+  std::vector<long long> landed(n);
+  unsigned long long c[6];
+  int flag = 0;
+  RB_CUDA(ctx, cudaMemcpyAsync(hit.data(), dev.hit.p, sizeof(double) * 2 * n,
+                               cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(landed.data(), dev.landed.p, sizeof(long long) * n,
+                               cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(c, dev.counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(&flag, k.err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaStreamSynchronize(st));
+  if (flag) return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+  int64_t landed_total = 0;
+  for (int64_t q = 0; q < n; ++q) {
+    if (out->hit_sum) {
+      out->hit_sum[2 * q] = hit[2 * q];
+      out->hit_sum[2 * q + 1] = hit[2 * q + 1];
+    }
+    if (out->landed) out->landed[q] = landed[q];
+    landed_total += landed[q];
+  }
+  fill_report(out, s, n, c, landed_total);
+  out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return RB_OK;
+}

@@ -95,7 +95,20 @@ struct KScene {
   int* err_flag;
 };
 
+// FP64 GriddedField nodes for the validation build (kernels_fp64.cu).
+struct Field64 {
+  const double *n, *gx, *gy, *gz;
+  int nx, ny, nz, pad;
+  double3 origin, spacing, lo, hi;
+};
+
 // ---- launches (all on `stream`) ----
+cudaError_t launch_trace_rays_fp64(const KScene& s, const Field64& f, int64_t n, const int64_t* src,
+                                   const int32_t* ray, double* uv, int32_t* status,
+                                   int32_t* steps, cudaStream_t stream);
+cudaError_t launch_source_stats_fp64(const KScene& s, const Field64& f, cudaStream_t stream);
+cudaError_t launch_build_fp64(const float* rho, int nx, int ny, int nz, double k, double3 spacing,
+                              double* n, double* gx, double* gy, double* gz, cudaStream_t stream);
 cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream);
 int render_occupancy(int* blocks_per_sm);
 cudaError_t launch_trace_rays(const KScene& s, int64_t n, const int64_t* src, const int32_t* ray,

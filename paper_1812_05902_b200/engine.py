@@ -141,7 +141,25 @@ class GpuTracer:
             _raise(self.lib, self.ctx, rc, "rb_image_from_fixed")
         return img
 
-    def trace_rays(self, scene: FlatScene, src, ray, with_field: bool = True):
+    def trace_rays_fp64(self, scene: FlatScene, src, ray, with_field: bool = True):
+        """FP64 validation build of the per-ray replay (rb_trace_rays_fp64)."""
+        return self.trace_rays(scene, src, ray, with_field, fp64=True)
+
+    def trace_stats_fp64(self, scene: FlatScene, with_field: bool = True) -> TraceResult:
+        """FP64 validation build of the per-source DotHitStats (rb_trace_stats_fp64)."""
+        s, keep = scene.to_c()
+        n = scene.n_sources
+        hit = np.zeros((n, 2))
+        landed = np.zeros(n, dtype=np.int64)
+        out = abi.TraceOut()
+        out.hit_sum = abi.dptr(hit) if n else None
+        out.landed = abi.i64ptr(landed) if n else None
+        rc = self.lib.rb_trace_stats_fp64(self.ctx, C.byref(s), int(with_field), C.byref(out))
+        if rc:
+            _raise(self.lib, self.ctx, rc, "rb_trace_stats_fp64")
+        return TraceResult(hit, landed, None, report_from(out))
+
+    def trace_rays(self, scene: FlatScene, src, ray, with_field: bool = True, fp64: bool = False):
         s, keep = scene.to_c()
         src = np.ascontiguousarray(src, dtype=np.int64)
         ray = np.ascontiguousarray(ray, dtype=np.int32)
@@ -149,7 +167,8 @@ class GpuTracer:
         uv = np.zeros((n, 2))
         status = np.zeros(n, dtype=np.int32)
         steps = np.zeros(n, dtype=np.int32)
-        rc = self.lib.rb_trace_rays(self.ctx, C.byref(s), int(with_field), n, abi.i64ptr(src),
+        fn = self.lib.rb_trace_rays_fp64 if fp64 else self.lib.rb_trace_rays
+        rc = fn(self.ctx, C.byref(s), int(with_field), n, abi.i64ptr(src),
                                     abi.i32ptr(ray), abi.dptr(uv), abi.i32ptr(status),
                                     abi.i32ptr(steps))
         if rc:
