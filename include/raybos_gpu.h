@@ -162,6 +162,13 @@ typedef struct rb_trace_out {
   /* instrumentation (not in the reference report) */
   int64_t total_steps;     /* sum of RK4 steps over all rays                   */
   double kernel_ms;        /* device time of the render kernel(s), max over devices */
+  /* optional render tail on device (render, engine.cpp:513-514): when
+   * `quantized` is non-NULL and accumulate_image is set, it receives
+   * quantize(image, bit_depth, gain) (sensor.cpp:124-135), W*H uint16 */
+  uint16_t* quantized;
+  double gain;
+  int32_t bit_depth;
+  int32_t reserved2;
 } rb_trace_out;
 
 typedef struct rb_ctx rb_ctx;
@@ -248,6 +255,15 @@ int rb_trace_rays_fp64(rb_ctx* ctx, const rb_scene* scene, int with_field, int64
  * in the reference's order (engine.cpp:112-137): hit_sum / landed / counters
  * bit-identical to the reference under the same sin/cos caveat.  No image. */
 int rb_trace_stats_fp64(rb_ctx* ctx, const rb_scene* scene, int with_field, rb_trace_out* out);
+
+/* trace_debug (engine.cpp:605-624): the per-step trajectory of one ray, as the
+ * StepObserver (grin.hpp:64-66) records it — (xi, r, t) after the volume entry,
+ * after every accepted RK4 step and at the cut-back exit — 7 doubles per record
+ * (xi, rx, ry, rz, tx, ty, tz).  Runs the FP64 validation build, so the records
+ * follow the reference's arithmetic.  *n_records receives the total count even
+ * when it exceeds max_records (only the first max_records are written). */
+int rb_trace_debug(rb_ctx* ctx, const rb_scene* scene, int64_t source_index, int32_t ray_index,
+                   double* records, int64_t max_records, int64_t* n_records);
 
 #ifdef __cplusplus
 }

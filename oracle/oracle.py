@@ -169,6 +169,8 @@ class Reference:
             lib.refshim_trace_rays.argtypes = [vp, C.c_int, C.c_int64, C.POINTER(C.c_int64),
                                                C.POINTER(C.c_int32), dp, C.POINTER(C.c_int32),
                                                C.POINTER(C.c_int32), dp, cp, sz]
+            lib.refshim_trace_debug.argtypes = [vp, C.c_int64, C.c_int32, dp, C.c_int64]
+            lib.refshim_trace_debug.restype = C.c_int64
             lib.refshim_quantize.argtypes = [dp, C.c_int64, C.c_int, C.c_double,
                                              C.POINTER(C.c_uint16), cp, sz]
             lib.refshim_bos_metrics.argtypes = [vp, dp, C.POINTER(C.c_int64), dp,
@@ -263,6 +265,12 @@ class Reference:
         if rc:
             raise RuntimeError(err.value.decode())
         return uv, status, steps, exit_state
+
+    def trace_debug(self, dot: int, ray: int, cap: int = 100000) -> np.ndarray:
+        """The reference trace_debug records (xi, r, t) of one ray, shape (n, 7)."""
+        rec = np.zeros((cap, 7))
+        n = self.lib().refshim_trace_debug(self.h, dot, ray, abi.dptr(rec), cap)
+        return rec[:min(n, cap)].copy()
 
     def bos_metrics(self, ref: TraceResult, grad: TraceResult):
         m = np.zeros(6)

@@ -421,6 +421,31 @@ int refshim_trace_rays(void* hv, int with_field, int64_t n, const int64_t* src,
   });
 }
 
+// trace_debug's records (engine.cpp:605-624) for (dot, ray) via the public
+// API: sample_aperture_points -> emit_rays -> trace_through_volume with a
+// StepObserver.  Writes up to cap records of 7 doubles; returns the count.
+int64_t refshim_trace_debug(void* hv, int64_t dot, int32_t ray, double* rec, int64_t cap) {
+  const raybos::SceneSetup& st = static_cast<Handle*>(hv)->setup;
+  const auto pts = raybos::sample_aperture_points(st.pupil, st.bundle, static_cast<std::uint64_t>(dot));
+  const auto rays = raybos::emit_rays(st.sources[dot], pts, st.wavelength);
+  int64_t n = 0;
+  raybos::StepObserver obs = [&](double xi, const raybos::RayState& s) {
+    if (n < cap) {
+      double* q = rec + 7 * n;
+      q[0] = xi;
+      q[1] = s.r.x;
+      q[2] = s.r.y;
+      q[3] = s.r.z;
+      q[4] = s.t.x;
+      q[5] = s.t.y;
+      q[6] = s.t.z;
+    }
+    ++n;
+  };
+  raybos::trace_through_volume(rays[ray], *st.field, st.step, &obs);
+  return n;
+}
+
 // quantize (sensor.cpp:124-135), for PGM byte-compatibility checks.
 int refshim_quantize(const double* img, int64_t n, int bit_depth, double gain, uint16_t* out,
                      char* err, size_t errlen) {

@@ -64,7 +64,8 @@ class TraceOut(C.Structure):
                 ("blocked_tir", C.c_int64), ("blocked_sensor_miss", C.c_int64),
                 ("wall_seconds", C.c_double), ("threads", C.c_int32), ("reserved", C.c_int32),
                 ("config_hash", C.c_uint64), ("total_steps", C.c_int64),
-                ("kernel_ms", C.c_double)]
+                ("kernel_ms", C.c_double), ("quantized", C.POINTER(C.c_uint16)),
+                ("gain", C.c_double), ("bit_depth", C.c_int32), ("reserved2", C.c_int32)]
 
 
 def vec3(v) -> Vec3:
@@ -105,7 +106,7 @@ EXPORTED_SYMBOLS = (
     "rb_create", "rb_destroy", "rb_last_error", "rb_abi_version", "rb_device_count",
     "rb_set_field_nodes", "rb_set_field_density", "rb_clear_field", "rb_field_bytes",
     "rb_trace", "rb_plan_shards", "rb_trace_shard", "rb_image_from_fixed", "rb_trace_rays",
-    "rb_trace_rays_fp64", "rb_trace_stats_fp64",
+    "rb_trace_rays_fp64", "rb_trace_stats_fp64", "rb_trace_debug",
 )
 
 _lib = None
@@ -160,6 +161,9 @@ def load_library(path: str | None = None) -> C.CDLL:
     lib.rb_trace_rays_fp64.restype = C.c_int
     lib.rb_trace_stats_fp64.argtypes = [C.c_void_p, C.POINTER(Scene), C.c_int, C.POINTER(TraceOut)]
     lib.rb_trace_stats_fp64.restype = C.c_int
+    lib.rb_trace_debug.argtypes = [C.c_void_p, C.POINTER(Scene), C.c_int64, C.c_int32,
+                                   C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int64)]
+    lib.rb_trace_debug.restype = C.c_int
     if lib.rb_abi_version() != RB_ABI_VERSION:
         raise RuntimeError("libraybos_gpu.so ABI version mismatch; rebuild")
     if path is None:

@@ -64,6 +64,7 @@ struct Device {
   Buf sources, ids, order, image, hit, landed, counters, queue, err, dimage, rays_src, rays_idx,
       rays_uv, rays_status, rays_steps;
   Buf f64[4];  // FP64 node copy (n, gx, gy, gz) for the validation build
+  Buf qimage, dbg, dbg_n;
 };
 
 struct NcclApi {
@@ -531,6 +532,7 @@ void rb_destroy(rb_ctx* ctx) {
     cudaSetDevice(d.ordinal);
     if (d.grid) cudaFree(d.grid);
     for (Buf& b : d.f64) b.release();
+    for (Buf* b : {&d.qimage, &d.dbg, &d.dbg_n}) b->release();
     for (Buf* b : {&d.sources, &d.ids, &d.order, &d.image, &d.hit, &d.landed, &d.counters,
                    &d.queue, &d.err, &d.dimage, &d.rays_src, &d.rays_idx, &d.rays_uv,
                    &d.rays_status, &d.rays_steps})
@@ -642,6 +644,12 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
   if (!ctx || !out) return RB_E_INVALID;
   const auto t0 = std::chrono::steady_clock::now();
   if (int rc = validate_scene(ctx, s)) return rc;
+  if (accumulate_image && out->quantized) {  // quantize's own checks, sensor.cpp:126-129
+    const int b = out->bit_depth;
+    if (b != 8 && b != 10 && b != 12 && b != 16)
+      return fail(ctx, RB_E_INVALID, "quantize: bit depth must be one of 8, 10, 12, 16");
+    if (!(out->gain > 0.0)) return fail(ctx, RB_E_INVALID, "quantize: gain must be positive");
+  }
   const int W = s->sensor.width_px, H = s->sensor.height_px;
   const size_t npx = static_cast<size_t>(W) * H;
   const int nd = static_cast<int>(ctx->devs.size());
@@ -649,6 +657,7 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
   out->kernel_ms = 0.0;
   if (s->n_sources == 0) {  // engine.cpp:436: one "thread", blank image, no stats
     if (accumulate_image && out->image) std::memset(out->image, 0, npx * sizeof(double));
+    if (accumulate_image && out->quantized) std::memset(out->quantized, 0, npx * sizeof(uint16_t));
     const unsigned long long zero[6] = {0, 0, 0, 0, 0, 0};
     fill_report(out, s, 0, zero, 0);
     out->threads = 1;
@@ -724,6 +733,14 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
                                             d0.stream));
     RB_CUDA(ctx, cudaMemcpyAsync(out->image, d0.dimage.p, npx * sizeof(double),
                                  cudaMemcpyDeviceToHost, d0.stream));
+    if (out->quantized) {  // render's quantize on device (sensor.cpp:124-135)
+      RB_CUDA(ctx, d0.qimage.ensure(npx * sizeof(uint16_t)));
+      RB_CUDA(ctx, rbk::launch_quantize(d0.dimage.as<double>(), static_cast<int64_t>(npx),
+                                        out->gain, out->bit_depth, d0.qimage.as<uint16_t>(),
+                                        d0.stream));
+      RB_CUDA(ctx, cudaMemcpyAsync(out->quantized, d0.qimage.p, npx * sizeof(uint16_t),
+                                   cudaMemcpyDeviceToHost, d0.stream));
+    }
     RB_CUDA(ctx, cudaStreamSynchronize(d0.stream));
   }
   fill_report(out, s, s->n_sources, c, landed_total);
@@ -990,5 +1007,37 @@ extern "C" int rb_trace_stats_fp64(rb_ctx* ctx, const rb_scene* s, int with_fiel
   }
   fill_report(out, s, n, c, landed_total);
   out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return RB_OK;
+}
+
+extern "C" int rb_trace_debug(rb_ctx* ctx, const rb_scene* s, int64_t source_index,
+                              int32_t ray_index, double* records, int64_t max_records,
+                              int64_t* n_records) {
+  if (!ctx || !n_records) return RB_E_INVALID;
+  if (int rc = validate_scene(ctx, s)) return rc;
+  // the reference's own checks, engine.cpp:607-612
+  if (!ctx->has_field) return fail(ctx, RB_E_RUNTIME, "trace_debug: config has no density field");
+  if (source_index < 0 || source_index >= s->n_sources)
+    return fail(ctx, RB_E_RUNTIME, "trace_debug: dot index out of range");
+  if (ray_index < 0 || ray_index >= s->rays_per_source)
+    return fail(ctx, RB_E_RUNTIME, "trace_debug: ray index out of range");
+  if (max_records < 0 || (max_records > 0 && !records)) return RB_E_INVALID;
+  Device& dev = ctx->devs[0];
+  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+  rbk::KScene k = make_kscene(ctx, s, 1, 0);
+  rbk::Field64 f;
+  if (int rc = field64(ctx, dev, 1, f)) return rc;
+  if (int rc = upload_scene_arrays(ctx, dev, s, k)) return rc;
+  RB_CUDA(ctx, dev.dbg.ensure(sizeof(double) * 7 * std::max<int64_t>(max_records, 1)));
+  RB_CUDA(ctx, dev.dbg_n.ensure(sizeof(int64_t)));
+  RB_CUDA(ctx, rbk::launch_trace_debug(k, f, source_index, ray_index, dev.dbg.as<double>(),
+                                       max_records, dev.dbg_n.as<int64_t>(), dev.stream));
+  int64_t n = 0;
+  RB_CUDA(ctx, cudaMemcpyAsync(&n, dev.dbg_n.p, sizeof(int64_t), cudaMemcpyDeviceToHost, dev.stream));
+  RB_CUDA(ctx, cudaStreamSynchronize(dev.stream));
+  const int64_t w = std::min(n, max_records);
+  if (w > 0)
+    RB_CUDA(ctx, cudaMemcpy(records, dev.dbg.p, sizeof(double) * 7 * w, cudaMemcpyDeviceToHost));
+  *n_records = n;
   return RB_OK;
 }

@@ -411,6 +411,17 @@ __global__ void image_finalize_kernel(const unsigned long long* __restrict__ fx,
     out[q] = (double)fx[q] * (1.0 / 2147483648.0);
 }
 
+// ------------------------------------------------ K3: quantize (render tail)
+// quantize, sensor.cpp:124-135: counts = llround(gain * v), clamped.
+__global__ void quantize_kernel(const double* __restrict__ img, int64_t n, double gain,
+                                long long max_count, uint16_t* __restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const long long c = llround(gain * img[q]);
+    out[q] = (uint16_t)(c < 0 ? 0 : (c > max_count ? max_count : c));
+  }
+}
+
 // ------------------------------------------------ launch wrappers
 static size_t render_smem() { return (size_t)kTileCap * sizeof(uint32_t); }
 
@@ -447,6 +458,13 @@ cudaError_t launch_build_from_density(const float* rho, int nx, int ny, int nz, 
                                       double3 spacing, float4* out, int z0, int z1,
                                       cudaStream_t stream) {
   build_from_density_kernel<<<148 * 8, 256, 0, stream>>>(rho, nx, ny, nz, k, spacing, out, z0, z1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const double* image, int64_t n, double gain, int bit_depth,
+                            uint16_t* out, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  quantize_kernel<<<148 * 4, 256, 0, stream>>>(image, n, gain, (1LL << bit_depth) - 1, out);
   return cudaGetLastError();
 }
 

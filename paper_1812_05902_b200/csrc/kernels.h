@@ -107,6 +107,10 @@ cudaError_t launch_trace_rays_fp64(const KScene& s, const Field64& f, int64_t n,
                                    const int32_t* ray, double* uv, int32_t* status,
                                    int32_t* steps, cudaStream_t stream);
 cudaError_t launch_source_stats_fp64(const KScene& s, const Field64& f, cudaStream_t stream);
+cudaError_t launch_trace_debug(const KScene& s, const Field64& f, int64_t src, int ray,
+                               double* rec, int64_t cap, int64_t* n_rec, cudaStream_t stream);
+cudaError_t launch_quantize(const double* image, int64_t n, double gain, int bit_depth,
+                            uint16_t* out, cudaStream_t stream);
 cudaError_t launch_build_fp64(const float* rho, int nx, int ny, int nz, double k, double3 spacing,
                               double* n, double* gx, double* gy, double* gz, cudaStream_t stream);
 cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream);

@@ -157,9 +157,29 @@ __device__ __forceinline__ bool contains64(const Field64& F, double3 p) {
          p.z <= F.hi.z;
 }
 
+// StepObserver (grin.hpp:64-66) sink for trace_debug: (xi, r, t) records.
+struct Recorder {
+  double* rec;
+  int64_t cap;
+  int64_t n;
+  __device__ void operator()(double xi, double3 r, double3 t) {
+    if (rec && n < cap) {
+      double* q = rec + 7 * n;
+      q[0] = xi;
+      q[1] = r.x;
+      q[2] = r.y;
+      q[3] = r.z;
+      q[4] = t.x;
+      q[5] = t.y;
+      q[6] = t.z;
+    }
+    ++n;
+  }
+};
+
 // trace_through_volume, grin.cpp:74-134, with rk4_step_impl (grin.cpp:35-44).
 __device__ int grin64(const Field64& F, double h, int max_steps, double3& o, double3& d,
-                      int& steps) {
+                      int& steps, Recorder* obs = nullptr) {
   steps = 0;
   double tn;
   if (!aabb64(F, o, d, tn)) return kMissed;
@@ -169,6 +189,8 @@ __device__ int grin64(const Field64& F, double h, int max_steps, double3& o, dou
   double ne;
   double3 ge;
   double3 t = d * (sample64(F, r, ne, ge) ? ne : 1.0);
+  double xi = 0.0;
+  if (obs) (*obs)(xi, r, t);
   for (int step = 0; step < max_steps; ++step) {
     const double3 a = clamped_d(F, r) * h;
     const double3 b = clamped_d(F, r + (t * 0.5 + a * 0.125) * h) * h;
@@ -183,6 +205,8 @@ __device__ int grin64(const Field64& F, double h, int max_steps, double3& o, dou
     if (contains64(F, nr)) {
       r = nr;
       t = nt;
+      xi += h;
+      if (obs) (*obs)(xi, r, t);
       continue;
     }
     double s = 1.0;
@@ -194,8 +218,12 @@ __device__ int grin64(const Field64& F, double h, int max_steps, double3& o, dou
       if (r1[ax] > hi[ax]) s = fmin(s, (hi[ax] - r0[ax]) / delta);
     }
     s = clampd(s, 0.0, 1.0);
-    o = r + (nr - r) * s;
-    d = normalized(t + (nt - t) * s);
+    const double3 er = r + (nr - r) * s;
+    const double3 et = t + (nt - t) * s;
+    xi += s * h;
+    if (obs) (*obs)(xi, er, et);
+    o = er;
+    d = normalized(et);
     steps = step + 1;
     return kTraced;
   }
@@ -274,6 +302,21 @@ __global__ void source_stats_fp64_kernel(const __grid_constant__ KScene S, const
     if (c[j]) atomicAdd(&S.counters[j], c[j]);
 }
 
+// trace_debug (engine.cpp:605-624): one ray, its trajectory records.
+__global__ void trace_debug_kernel(const __grid_constant__ KScene S, const Field64 F, int64_t src,
+                                   int ray, double* rec, int64_t cap, int64_t* n_rec) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
+  const double3 so = make_double3(S.sources[3 * src], S.sources[3 * src + 1], S.sources[3 * src + 2]);
+  const double3 p = aperture_point(S, mix_bits(S.key_seed + sid), ray);
+  const double3 to = p - so;
+  double3 o = so, d = to / norm(to);
+  Recorder obs{rec, cap, 0};
+  int steps = 0;
+  grin64(F, S.h, S.max_steps, o, d, steps, &obs);
+  *n_rec = obs.n;
+}
+
 // FP64 GriddedField nodes from the density volume (scene.cpp:53-92), the same
 // explicitly-rounded arithmetic as K0's float4 build.
 __device__ __forceinline__ double n_of64(const float* rho, double k, size_t q) {
@@ -323,6 +366,12 @@ cudaError_t launch_trace_rays_fp64(const KScene& s, const Field64& f, int64_t n,
 cudaError_t launch_source_stats_fp64(const KScene& s, const Field64& f, cudaStream_t stream) {
   if (s.n_sources <= 0) return cudaSuccess;
   source_stats_fp64_kernel<<<(unsigned)((s.n_sources + 63) / 64), 64, 0, stream>>>(s, f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace_debug(const KScene& s, const Field64& f, int64_t src, int ray,
+                               double* rec, int64_t cap, int64_t* n_rec, cudaStream_t stream) {
+  trace_debug_kernel<<<1, 32, 0, stream>>>(s, f, src, ray, rec, cap, n_rec);
   return cudaGetLastError();
 }
 

@@ -92,7 +92,9 @@ class GpuTracer:
 
     # ---- run_trace -----------------------------------------------------------
     def run_trace(self, scene: FlatScene, with_field: bool = True, accumulate_image: bool = True,
-                  image_out: Optional[np.ndarray] = None) -> TraceResult:
+                  image_out: Optional[np.ndarray] = None, quantize=None) -> TraceResult:
+        """rb_trace.  quantize=(bit_depth, gain) also returns the render tail's
+        quantized uint16 image (computed on device) as result.quantized."""
         s, keep = scene.to_c()
         n = scene.n_sources
         hit = np.zeros((n, 2))
@@ -105,11 +107,30 @@ class GpuTracer:
         out.hit_sum = abi.dptr(hit) if n else None
         out.landed = abi.i64ptr(landed) if n else None
         out.image = abi.dptr(img) if img is not None else None
+        qimg = None
+        if quantize is not None and accumulate_image:
+            qimg = np.zeros((scene.height, scene.width), dtype=np.uint16)
+            out.quantized = qimg.ctypes.data_as(C.POINTER(C.c_uint16))
+            out.bit_depth, out.gain = int(quantize[0]), float(quantize[1])
         rc = self.lib.rb_trace(self.ctx, C.byref(s), int(with_field), int(accumulate_image),
                                C.byref(out))
         if rc:
             _raise(self.lib, self.ctx, rc, "rb_trace")
-        return TraceResult(hit, landed, img, report_from(out))
+        res = TraceResult(hit, landed, img, report_from(out))
+        res.quantized = qimg
+        return res
+
+    def trace_debug(self, scene: FlatScene, source_index: int, ray_index: int,
+                    max_records: int = 100000) -> np.ndarray:
+        """rb_trace_debug: StepObserver records (xi, r, t) of one ray, shape (n, 7)."""
+        s, keep = scene.to_c()
+        rec = np.zeros((max_records, 7))
+        n = C.c_int64()
+        rc = self.lib.rb_trace_debug(self.ctx, C.byref(s), int(source_index), int(ray_index),
+                                     abi.dptr(rec), max_records, C.byref(n))
+        if rc:
+            _raise(self.lib, self.ctx, rc, "rb_trace_debug")
+        return rec[:min(n.value, max_records)].copy()
 
     def trace_shard(self, scene: FlatScene, with_field: bool, accumulate_image: bool,
                     shard_index: int, shard_count: int, image_fixed_ptr: int,

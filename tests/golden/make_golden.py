@@ -152,6 +152,12 @@ def make(name, spec, n_ray_samples=2048):
     out["ray_src"], out["ray_idx"] = src, ray
     out["info"] = np.array([info.magnification, info.f_number, info.gain, info.d_tau,
                             info.lens_plane_z, info.focal_length])
+    if field is not None:  # trace_debug records for a few rays (engine.cpp:605-624)
+        dbg = [(0, 0), (scene.n_sources // 2, scene.rays_per_source // 2),
+               (scene.n_sources - 1, scene.rays_per_source - 1)]
+        out["debug_rays"] = np.array(dbg, dtype=np.int64)
+        for k, (d_, r_) in enumerate(dbg):
+            out[f"debug_{k}"] = ref.trace_debug(d_, r_)
     for wf in (1, 0):
         uv, status, steps, exit_state = ref.trace_rays(src, ray, with_field=bool(wf))
         out[f"ray_uv_{wf}"], out[f"ray_status_{wf}"], out[f"ray_steps_{wf}"] = uv, status, steps

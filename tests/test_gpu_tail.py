@@ -1,0 +1,52 @@
+"""SURVEY §8(f) rows on the GPU: f4 trace_debug records (engine.cpp:605-624) and
+f3 the render tail's quantize (sensor.cpp:124-135) computed on device."""
+import numpy as np
+import pytest
+
+from golden_io import NAMES, load
+
+pytestmark = pytest.mark.gpu
+
+FIELD_FIXTURES = [n for n in NAMES if "debug_rays" in load(n)[2]]
+
+
+@pytest.mark.parametrize("name", FIELD_FIXTURES)
+def test_trace_debug_records_match_reference(tracer, name):
+    scene, field, g = load(name)
+    tracer.set_field(field)
+    for k, (dot, ray) in enumerate(g["debug_rays"]):
+        ref = g[f"debug_{k}"]
+        got = tracer.trace_debug(scene, int(dot), int(ray))
+        assert got.shape == ref.shape
+        # FP64 validation arithmetic: bit-exact unless glibc's sin/cos of this ray's
+        # aperture angle is not correctly rounded (test_sincos_rounding.py)
+        scale = np.abs(ref).max(axis=0).clip(1e-30)
+        assert (np.abs(got - ref) / scale).max() < 1e-13
+        assert np.all(np.diff(got[:, 0]) > 0)  # xi increases (test_engine.cpp:217-221)
+
+
+def test_trace_debug_errors(tracer):
+    scene, field, g = load("small")
+    tracer.set_field(field)
+    with pytest.raises(Exception, match="dot index out of range"):
+        tracer.trace_debug(scene, 9999, 0)
+    with pytest.raises(Exception, match="ray index out of range"):
+        tracer.trace_debug(scene, 0, 9999)
+    tracer.set_field(None)
+    with pytest.raises(Exception, match="no density field"):
+        tracer.trace_debug(scene, 0, 0)
+
+
+@pytest.mark.parametrize("name", ["small", "singlet_defocus", "blob"])
+@pytest.mark.parametrize("bits", [16, 12, 8])
+def test_device_quantize_matches_host_quantize(tracer, name, bits):
+    from paper_1812_05902_b200 import setup as S
+    scene, field, g = load(name)
+    tracer.set_field(field)
+    gain = 0.9 * ((1 << bits) - 1) / g["image_1"].max()
+    res = tracer.run_trace(scene, True, True, quantize=(bits, gain))
+    # same FP64 image -> identical counts (llround, clamp), as render would write them
+    assert np.array_equal(res.quantized, S.quantize(res.image, bits, gain))
+    # and within one count of quantizing the reference's own image
+    ref_q = S.quantize(g["image_1"], bits, gain).astype(np.int64)
+    assert np.abs(res.quantized.astype(np.int64) - ref_q).max() <= 1
