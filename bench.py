@@ -115,6 +115,16 @@ def measure_peaks(device: int) -> dict:
             "l2_gather_gbs": lib.rbp_l2_gather_gbs(device, 64.0)}
 
 
+def profiled_traffic(scene: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch of this
+    scene, from the committed ncu capture (profiles/k1_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            return json.load(f).get(scene, {}).get("dram_bytes_per_launch")
+    except OSError:
+        return None
+
+
 def measured_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -347,7 +357,9 @@ def main_ours(args, rank, world, local):
     achieved = flops / (kms * 1e-3) / 1e12
     gather = GATHER_BYTES_PER_STEP * steps_sum / (kms * 1e-3) / 1e9
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peaks["ffma_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["ffma_tflops"], "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / peaks["ffma_tflops"],
+                "traffic": profiled_traffic(args.scene) if world == 1 else None,
+                "traffic_source": "profiles/k1_traffic.json (ncu --set full, one launch)",
                 "kernel": "render_emitters", "kernel_ms": kms,
                 "peak_source": "measured on this box: FFMA microbenchmark (tools/peaks.cu), "
                                "max of register/immediate operand forms",
