@@ -256,6 +256,15 @@ int rb_trace_rays_fp64(rb_ctx* ctx, const rb_scene* scene, int with_field, int64
  * bit-identical to the reference under the same sin/cos caveat.  No image. */
 int rb_trace_stats_fp64(rb_ctx* ctx, const rb_scene* scene, int with_field, rb_trace_out* out);
 
+/* bos_run's two traces (engine.cpp:539-540: run_trace without, then with the
+ * field, identical seeds) fused into one pass: every ray is generated once and
+ * followed both straight (reference leg) and through the density grid
+ * (gradient leg).  Per-dot DotHitStats and counters for both legs, no images
+ * (bos_run only needs images when write_images is set; use rb_trace for those).
+ * Bit-identical to two rb_trace(accumulate_image = 0) calls. */
+int rb_trace_bos_pair(rb_ctx* ctx, const rb_scene* scene, rb_trace_out* out_reference,
+                      rb_trace_out* out_gradient);
+
 /* trace_debug (engine.cpp:605-624): the per-step trajectory of one ray, as the
  * StepObserver (grin.hpp:64-66) records it — (xi, r, t) after the volume entry,
  * after every accepted RK4 step and at the cut-back exit — 7 doubles per record

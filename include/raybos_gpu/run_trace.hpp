@@ -28,6 +28,7 @@
 #include <stdexcept>
 #include <string>
 #include <type_traits>
+#include <utility>
 #include <variant>
 #include <vector>
 
@@ -108,18 +109,19 @@ inline Context& context() {
 
 }  // namespace detail
 
-// The reference's run_trace contract on B200 (engine.hpp:73-78).
-inline raybos::TraceOutputs run_trace(const raybos::SceneSetup& setup, bool with_field,
-                                      bool accumulate_image, const raybos::RunConfig& run) {
-  (void)run;  // threads / deterministic: see header comment
-  detail::Context& C = detail::context();
-  std::lock_guard<std::mutex> lock(C.mu);
-  if (with_field && setup.field) C.ensure_field(setup.field);
+namespace detail {
 
+// SceneSetup -> rb_scene (engine.hpp:40-60); the vectors back the pointers.
+struct FlatScene {
   std::vector<rb_vec3> sources;
-  sources.reserve(setup.sources.size());
-  for (const raybos::Vec3& s : setup.sources) sources.push_back(detail::v3(s));
   std::vector<rb_element> elements;
+  rb_scene s{};
+};
+
+inline void flatten(const raybos::SceneSetup& setup, FlatScene& f) {
+  f.sources.clear();
+  for (const raybos::Vec3& v : setup.sources) f.sources.push_back(v3(v));
+  f.elements.clear();
   for (const raybos::OpticalElement& e : setup.elements) {
     rb_element r{};
     std::visit(
@@ -127,33 +129,34 @@ inline raybos::TraceOutputs run_trace(const raybos::SceneSetup& setup, bool with
           using T = std::decay_t<decltype(x)>;
           if constexpr (std::is_same_v<T, raybos::Aperture>) {
             r.kind = RB_ELEM_APERTURE;
-            r.center = detail::v3(x.center);
-            r.axis = detail::v3(x.normal);
+            r.center = v3(x.center);
+            r.axis = v3(x.normal);
             r.radius = x.radius;
           } else if constexpr (std::is_same_v<T, raybos::LensElement>) {
             r.kind = RB_ELEM_SINGLET;
-            r.front = detail::surf(x.front);
-            r.back = detail::surf(x.back);
+            r.front = surf(x.front);
+            r.back = surf(x.back);
             r.diameter = x.diameter;
           } else if constexpr (std::is_same_v<T, raybos::ThinLensIdeal>) {
             r.kind = RB_ELEM_THIN_LENS;
-            r.center = detail::v3(x.center);
-            r.axis = detail::v3(x.axis);
+            r.center = v3(x.center);
+            r.axis = v3(x.axis);
             r.focal_length = x.focal_length;
             r.diameter = x.diameter;
           } else {
             r.kind = RB_ELEM_MIRROR;
-            r.front = detail::surf(x.surface);
+            r.front = surf(x.surface);
           }
         },
         e);
-    elements.push_back(r);
+    f.elements.push_back(r);
   }
-  rb_scene s{};
-  s.sources = sources.data();
-  s.n_sources = static_cast<int64_t>(sources.size());
-  s.pupil_center = detail::v3(setup.pupil.center);
-  s.pupil_axis = detail::v3(setup.pupil.axis);
+  rb_scene& s = f.s;
+  s = rb_scene{};
+  s.sources = f.sources.data();
+  s.n_sources = static_cast<int64_t>(f.sources.size());
+  s.pupil_center = v3(setup.pupil.center);
+  s.pupil_axis = v3(setup.pupil.axis);
   s.pupil_radius = setup.pupil.radius;
   s.rays_per_source = setup.bundle.rays_per_source;
   s.sampling = setup.bundle.sampling == raybos::ApertureSampling::kStratified
@@ -163,31 +166,25 @@ inline raybos::TraceOutputs run_trace(const raybos::SceneSetup& setup, bool with
   s.wavelength = setup.wavelength;
   s.delta_xi = setup.step.delta_xi;
   s.max_steps = setup.step.max_steps;
-  s.n_elements = static_cast<int32_t>(elements.size());
-  s.elements = elements.data();
-  s.sensor.center = detail::v3(setup.sensor.center);
-  s.sensor.normal = detail::v3(setup.sensor.normal);
-  s.sensor.e_u = detail::v3(setup.sensor.e_u);
-  s.sensor.e_v = detail::v3(setup.sensor.e_v);
+  s.n_elements = static_cast<int32_t>(f.elements.size());
+  s.elements = f.elements.data();
+  s.sensor.center = v3(setup.sensor.center);
+  s.sensor.normal = v3(setup.sensor.normal);
+  s.sensor.e_u = v3(setup.sensor.e_u);
+  s.sensor.e_v = v3(setup.sensor.e_v);
   s.sensor.width_px = setup.sensor.width_px;
   s.sensor.height_px = setup.sensor.height_px;
   s.sensor.pitch = setup.sensor.pitch;
   s.sensor.window_sigmas = setup.sensor.window_sigmas;
   s.d_tau = setup.d_tau;
   s.config_hash = setup.config_hash;
+}
 
-  raybos::TraceOutputs out;
-  out.stats.resize(setup.sources.size());
-  std::vector<double> hit(2 * setup.sources.size());
-  std::vector<int64_t> landed(setup.sources.size());
-  if (accumulate_image) out.image = raybos::ImageBuffer(setup.sensor.width_px, setup.sensor.height_px);
-  rb_trace_out o{};
-  o.hit_sum = hit.data();
-  o.landed = landed.data();
-  o.image = accumulate_image ? out.image.data.data() : nullptr;
-  const int rc = rb_trace(C.ctx, &s, (with_field && setup.field) ? 1 : 0, accumulate_image ? 1 : 0, &o);
-  if (rc) detail::raise(rc, rb_last_error(C.ctx));
-  for (size_t d = 0; d < out.stats.size(); ++d) {
+// rb_trace_out -> TraceOutputs / RunReport (engine.hpp:19-36, 67-71).
+inline void unflatten(const rb_trace_out& o, const std::vector<double>& hit,
+                      const std::vector<int64_t>& landed, raybos::TraceOutputs& out) {
+  out.stats.resize(landed.size());
+  for (size_t d = 0; d < landed.size(); ++d) {
     out.stats[d].hit_sum = {hit[2 * d], hit[2 * d + 1]};
     out.stats[d].landed = static_cast<long>(landed[d]);
   }
@@ -202,6 +199,58 @@ inline raybos::TraceOutputs run_trace(const raybos::SceneSetup& setup, bool with
   r.wall_seconds = o.wall_seconds;
   r.threads = o.threads;
   r.config_hash = o.config_hash;
+}
+
+}  // namespace detail
+
+// The reference's run_trace contract on B200 (engine.hpp:73-78).
+inline raybos::TraceOutputs run_trace(const raybos::SceneSetup& setup, bool with_field,
+                                      bool accumulate_image, const raybos::RunConfig& run) {
+  (void)run;  // threads / deterministic: see header comment
+  detail::Context& C = detail::context();
+  std::lock_guard<std::mutex> lock(C.mu);
+  if (with_field && setup.field) C.ensure_field(setup.field);
+  detail::FlatScene f;
+  detail::flatten(setup, f);
+  raybos::TraceOutputs out;
+  std::vector<double> hit(2 * setup.sources.size());
+  std::vector<int64_t> landed(setup.sources.size());
+  if (accumulate_image) out.image = raybos::ImageBuffer(setup.sensor.width_px, setup.sensor.height_px);
+  rb_trace_out o{};
+  o.hit_sum = hit.data();
+  o.landed = landed.data();
+  o.image = accumulate_image ? out.image.data.data() : nullptr;
+  const int rc = rb_trace(C.ctx, &f.s, (with_field && setup.field) ? 1 : 0, accumulate_image ? 1 : 0, &o);
+  if (rc) detail::raise(rc, rb_last_error(C.ctx));
+  detail::unflatten(o, hit, landed, out);
+  return out;
+}
+
+// bos_run's two traces (engine.cpp:539-540, write_images off) in one fused
+// pass: {run_trace(setup, false, false, run), run_trace(setup, true, false, run)},
+// bit-identical to the two separate calls.
+inline std::pair<raybos::TraceOutputs, raybos::TraceOutputs> run_trace_bos_pair(
+    const raybos::SceneSetup& setup, const raybos::RunConfig& run) {
+  (void)run;
+  if (!setup.field) throw std::runtime_error("bos_run: config must include a density field");
+  detail::Context& C = detail::context();
+  std::lock_guard<std::mutex> lock(C.mu);
+  C.ensure_field(setup.field);
+  detail::FlatScene f;
+  detail::flatten(setup, f);
+  const size_t n = setup.sources.size();
+  std::vector<double> h0(2 * n), h1(2 * n);
+  std::vector<int64_t> l0(n), l1(n);
+  rb_trace_out o0{}, o1{};
+  o0.hit_sum = h0.data();
+  o0.landed = l0.data();
+  o1.hit_sum = h1.data();
+  o1.landed = l1.data();
+  const int rc = rb_trace_bos_pair(C.ctx, &f.s, &o0, &o1);
+  if (rc) detail::raise(rc, rb_last_error(C.ctx));
+  std::pair<raybos::TraceOutputs, raybos::TraceOutputs> out;
+  detail::unflatten(o0, h0, l0, out.first);
+  detail::unflatten(o1, h1, l1, out.second);
   return out;
 }
 

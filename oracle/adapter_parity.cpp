@@ -91,10 +91,14 @@ void compare_bos(const std::string& name, const ExperimentConfig& cfg) {
   RunConfig run;
   FieldMetrics m[2];
   for (int impl = 0; impl < 2; ++impl) {
-    const TraceOutputs r0 = impl ? raybos_gpu::run_trace(setup, false, false, run)
-                                 : raybos::run_trace(setup, false, false, run);
-    const TraceOutputs r1 = impl ? raybos_gpu::run_trace(setup, true, false, run)
-                                 : raybos::run_trace(setup, true, false, run);
+    // impl 1: the fused drop-in (one pass, both legs)
+    std::pair<TraceOutputs, TraceOutputs> legs;
+    if (impl)
+      legs = raybos_gpu::run_trace_bos_pair(setup, run);
+    else
+      legs = {raybos::run_trace(setup, false, false, run), raybos::run_trace(setup, true, false, run)};
+    const TraceOutputs& r0 = legs.first;
+    const TraceOutputs& r1 = legs.second;
     const double shrink = 1.0 - setup.volume_center_z / setup.pupil.center.z;
     std::vector<Vec2> attach(setup.dot_positions.size());
     for (size_t d = 0; d < attach.size(); ++d) attach[d] = setup.dot_positions[d] * shrink;

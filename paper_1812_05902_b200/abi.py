@@ -106,7 +106,7 @@ EXPORTED_SYMBOLS = (
     "rb_create", "rb_destroy", "rb_last_error", "rb_abi_version", "rb_device_count",
     "rb_set_field_nodes", "rb_set_field_density", "rb_clear_field", "rb_field_bytes",
     "rb_trace", "rb_plan_shards", "rb_trace_shard", "rb_image_from_fixed", "rb_trace_rays",
-    "rb_trace_rays_fp64", "rb_trace_stats_fp64", "rb_trace_debug",
+    "rb_trace_rays_fp64", "rb_trace_stats_fp64", "rb_trace_debug", "rb_trace_bos_pair",
 )
 
 _lib = None
@@ -164,6 +164,9 @@ def load_library(path: str | None = None) -> C.CDLL:
     lib.rb_trace_debug.argtypes = [C.c_void_p, C.POINTER(Scene), C.c_int64, C.c_int32,
                                    C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int64)]
     lib.rb_trace_debug.restype = C.c_int
+    lib.rb_trace_bos_pair.argtypes = [C.c_void_p, C.POINTER(Scene), C.POINTER(TraceOut),
+                                      C.POINTER(TraceOut)]
+    lib.rb_trace_bos_pair.restype = C.c_int
     if lib.rb_abi_version() != RB_ABI_VERSION:
         raise RuntimeError("libraybos_gpu.so ABI version mismatch; rebuild")
     if path is None:

@@ -65,6 +65,7 @@ struct Device {
       rays_uv, rays_status, rays_steps;
   Buf f64[4];  // FP64 node copy (n, gx, gy, gz) for the validation build
   Buf qimage, dbg, dbg_n;
+  Buf hit0, landed0, counters0;  // bos pair mode: the no-field leg
 };
 
 struct NcclApi {
@@ -314,9 +315,10 @@ std::vector<int32_t> shard_list(const std::vector<int32_t>& z, int64_t index, in
 }
 
 struct PartialOut {
-  std::vector<double> hit;
-  std::vector<long long> landed;
+  std::vector<double> hit, hit0;
+  std::vector<long long> landed, landed0;
   unsigned long long counters[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long counters0[6] = {0, 0, 0, 0, 0, 0};
   float ms = 0.f;
   int err_flag = 0;
 };
@@ -357,6 +359,15 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   k.hit_sum = dev.hit.as<double>();
   k.landed = dev.landed.as<long long>();
   k.counters = dev.counters.as<unsigned long long>();
+  if (k.pair) {
+    RB_CUDA(ctx, dev.hit0.ensure(sizeof(double) * 2 * n));
+    RB_CUDA(ctx, dev.landed0.ensure(sizeof(long long) * n));
+    RB_CUDA(ctx, dev.counters0.ensure(sizeof(unsigned long long) * 8));
+    RB_CUDA(ctx, cudaMemsetAsync(dev.counters0.p, 0, sizeof(unsigned long long) * 8, st));
+    k.hit_sum0 = dev.hit0.as<double>();
+    k.landed0 = dev.landed0.as<long long>();
+    k.counters0 = dev.counters0.as<unsigned long long>();
+  }
   k.queue = dev.queue.as<int>();
   k.err_flag = dev.queue.as<int>() + 1;
   k.grid = dev.grid;
@@ -385,6 +396,18 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   }
   RB_CUDA(ctx, cudaMemcpyAsync(po.counters, dev.counters.p, sizeof(unsigned long long) * 6,
                                cudaMemcpyDeviceToHost, st));
+  if (k.pair) {
+    po.hit0.assign(2 * n, 0.0);
+    po.landed0.assign(n, 0);
+    if (n) {
+      RB_CUDA(ctx, cudaMemcpyAsync(po.hit0.data(), dev.hit0.p, sizeof(double) * 2 * n,
+                                   cudaMemcpyDeviceToHost, st));
+      RB_CUDA(ctx, cudaMemcpyAsync(po.landed0.data(), dev.landed0.p, sizeof(long long) * n,
+                                   cudaMemcpyDeviceToHost, st));
+    }
+    RB_CUDA(ctx, cudaMemcpyAsync(po.counters0, dev.counters0.p, sizeof(unsigned long long) * 6,
+                                 cudaMemcpyDeviceToHost, st));
+  }
   RB_CUDA(ctx, cudaMemcpyAsync(&po.err_flag, k.err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   RB_CUDA(ctx, cudaStreamSynchronize(st));
   RB_CUDA(ctx, cudaEventElapsedTime(&po.ms, dev.ev0, dev.ev1));
@@ -532,7 +555,7 @@ void rb_destroy(rb_ctx* ctx) {
     cudaSetDevice(d.ordinal);
     if (d.grid) cudaFree(d.grid);
     for (Buf& b : d.f64) b.release();
-    for (Buf* b : {&d.qimage, &d.dbg, &d.dbg_n}) b->release();
+    for (Buf* b : {&d.qimage, &d.dbg, &d.dbg_n, &d.hit0, &d.landed0, &d.counters0}) b->release();
     for (Buf* b : {&d.sources, &d.ids, &d.order, &d.image, &d.hit, &d.landed, &d.counters,
                    &d.queue, &d.err, &d.dimage, &d.rays_src, &d.rays_idx, &d.rays_uv,
                    &d.rays_status, &d.rays_steps})
@@ -1039,5 +1062,74 @@ extern "C" int rb_trace_debug(rb_ctx* ctx, const rb_scene* s, int64_t source_ind
   if (w > 0)
     RB_CUDA(ctx, cudaMemcpy(records, dev.dbg.p, sizeof(double) * 7 * w, cudaMemcpyDeviceToHost));
   *n_records = n;
+  return RB_OK;
+}
+
+extern "C" int rb_trace_bos_pair(rb_ctx* ctx, const rb_scene* s, rb_trace_out* out_ref,
+                                 rb_trace_out* out_grad) {
+  if (!ctx || !out_ref || !out_grad) return RB_E_INVALID;
+  const auto t0 = std::chrono::steady_clock::now();
+  if (int rc = validate_scene(ctx, s)) return rc;
+  if (!ctx->has_field) return fail(ctx, RB_E_RUNTIME, "bos_run: config must include a density field");
+  const unsigned long long zero[6] = {0, 0, 0, 0, 0, 0};
+  if (s->n_sources == 0) {
+    fill_report(out_ref, s, 0, zero, 0);
+    fill_report(out_grad, s, 0, zero, 0);
+    out_ref->threads = out_grad->threads = 1;
+    return RB_OK;
+  }
+  rbk::KScene base = make_kscene(ctx, s, 1, 0);
+  base.pair = 1;
+  const std::vector<int32_t> z = zorder(s);
+  const int nd = static_cast<int>(ctx->devs.size());
+  const int used = static_cast<int>(std::min<int64_t>(nd, (s->n_sources + kShardTile - 1) / kShardTile));
+  std::vector<PartialOut> parts(used);
+  std::vector<int> rcs(used, RB_OK);
+  std::vector<std::vector<int32_t>> work(used);
+  for (int d = 0; d < used; ++d) work[d] = shard_list(z, d, used);
+  if (used == 1) {
+    rcs[0] = render_on(ctx, ctx->devs[0], s, base, work[0], nullptr, parts[0]);
+  } else {
+    std::vector<std::thread> pool;
+    for (int d = 0; d < used; ++d)
+      pool.emplace_back([&, d] { rcs[d] = render_on(ctx, ctx->devs[d], s, base, work[d], nullptr, parts[d]); });
+    for (auto& t : pool) t.join();
+  }
+  for (int d = 0; d < used; ++d)
+    if (rcs[d]) return rcs[d];
+  for (int d = 0; d < used; ++d)
+    if (parts[d].err_flag)
+      return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0}, c0[6] = {0, 0, 0, 0, 0, 0};
+  int64_t lt = 0, lt0 = 0;
+  float ms = 0.f;
+  for (int d = 0; d < used; ++d) {
+    for (int j = 0; j < 6; ++j) {
+      c[j] += parts[d].counters[j];
+      c0[j] += parts[d].counters0[j];
+    }
+    ms = std::max(ms, parts[d].ms);
+    for (int32_t src : work[d]) {
+      if (out_grad->hit_sum) {
+        out_grad->hit_sum[2 * src] = parts[d].hit[2 * src];
+        out_grad->hit_sum[2 * src + 1] = parts[d].hit[2 * src + 1];
+      }
+      if (out_grad->landed) out_grad->landed[src] = parts[d].landed[src];
+      if (out_ref->hit_sum) {
+        out_ref->hit_sum[2 * src] = parts[d].hit0[2 * src];
+        out_ref->hit_sum[2 * src + 1] = parts[d].hit0[2 * src + 1];
+      }
+      if (out_ref->landed) out_ref->landed[src] = parts[d].landed0[src];
+      lt += parts[d].landed[src];
+      lt0 += parts[d].landed0[src];
+    }
+  }
+  c0[5] = 0;  // no RK4 steps on the reference leg
+  fill_report(out_grad, s, s->n_sources, c, lt);
+  fill_report(out_ref, s, s->n_sources, c0, lt0);
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  out_ref->threads = out_grad->threads = used;
+  out_ref->kernel_ms = out_grad->kernel_ms = ms;
+  out_ref->wall_seconds = out_grad->wall_seconds = wall;
   return RB_OK;
 }

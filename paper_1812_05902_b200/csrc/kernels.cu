@@ -26,21 +26,28 @@ struct RayResult {
 };
 
 // process_source's per-ray body, engine.cpp:112-137.
-__device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, double3 src, int i,
-                                               double* scratch) {
-  RayResult r;
-  r.steps = 0;
-  r.u = r.v = 0.0;
+// emit_rays (raygen.cpp:74-80) for one ray: false when the source coincides
+// with its aperture point (the reference throws).
+__device__ __forceinline__ bool emit_ray(const KScene& S, uint64_t ekey, double3 src, int i,
+                                         double3& d) {
   const double3 p = aperture_point(S, ekey, i);
   const double3 to = p - src;
   const double len = norm(to);
-  if (!(len > 0.0)) {  // emit_rays: source coincides with aperture point (raygen.cpp:77)
+  if (!(len > 0.0)) {
     atomicOr(S.err_flag, 1);
-    r.status = 1;
-    return r;
+    return false;
   }
-  double3 o = src, d = to / len;
-  if (S.with_field) {
+  d = to / len;
+  return true;
+}
+
+// Stages 2-4 of process_source (engine.cpp:112-137) for an emitted ray.
+__device__ __forceinline__ RayResult finish_ray(const KScene& S, double3 o, double3 d, bool field,
+                                                double* scratch) {
+  RayResult r;
+  r.steps = 0;
+  r.u = r.v = 0.0;
+  if (field) {
     const int st = grin_trace(S, o, d, r.steps, scratch);
     if (st == kLost || st == kInvalid) {
       r.status = 1;  // RB_RAY_LOST
@@ -58,6 +65,20 @@ __device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, d
   }
   r.status = 0;
   return r;
+}
+
+// process_source's per-ray body, engine.cpp:112-137.
+__device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, double3 src, int i,
+                                               double* scratch) {
+  double3 d;
+  if (!emit_ray(S, ekey, src, i, d)) {
+    RayResult r;
+    r.u = r.v = 0.0;
+    r.steps = 0;
+    r.status = 1;
+    return r;
+  }
+  return finish_ray(S, src, d, S.with_field, scratch);
 }
 
 // Tile-or-global fixed-point add of one pixel contribution.
@@ -184,6 +205,9 @@ __device__ __forceinline__ T warp_sum(T v) {
 // pilot before any deposit so the CTA can place the emitter's shared-memory
 // tile over the pilot spots' bounding box (the pilot rays are spread over the
 // whole pupil lattice).  Deposits outside the tile go straight to global.
+// kPair: bos_run pair mode (rb_trace_bos_pair), a separate instantiation so the
+// default kernel carries none of its code or registers.
+template <bool kPair>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __grid_constant__ KScene S) {
   extern __shared__ uint32_t tile[];
   constexpr int kWarps = kBlock / 32;
@@ -200,6 +224,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
   __shared__ double sh_rt[kBlock][7];        // R0, T0 of the ray in flight (grin.cuh)
   __shared__ double sh_d[2][kWarps];
   __shared__ unsigned long long sh_l[7][kWarps];
+  // bos_run pair mode (rb_trace_bos_pair): the no-field leg's accumulators
+  __shared__ double sh_uv0[2][kBlock];
+  __shared__ unsigned sh_cnt0[7][kBlock];
+  __shared__ double sh_d0[2][kWarps];
+  __shared__ unsigned long long sh_l0[7][kWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = S.rays;
   const int K = (S.patch_count + kWarps - 1) / kWarps;
@@ -224,8 +253,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
       sh_tile[0] = sh_tile[1] = sh_tile[2] = sh_tile[3] = 0;
     }
     sh_uv[0][tid] = sh_uv[1][tid] = 0.0;
+    sh_uv0[0][tid] = sh_uv0[1][tid] = 0.0;
 #pragma unroll
-    for (int j = 0; j < 7; ++j) sh_cnt[j][tid] = 0u;
+    for (int j = 0; j < 7; ++j) sh_cnt[j][tid] = sh_cnt0[j][tid] = 0u;
     __syncthreads();
     if (sh_work >= S.n_work) break;
 
@@ -244,7 +274,26 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
       const uint64_t ekey = *vkey;
       RayResult r;
       r.status = -1;
-      if (i >= 0) r = trace_ray(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid]);
+      if (i >= 0) {
+        if (kPair) {  // one emitted ray, both legs: no field first (cheap), then the field
+          const double3 so = make_double3(vso[0], vso[1], vso[2]);
+          double3 d;
+          if (emit_ray(S, ekey, so, i, d)) {
+            const RayResult r0 = finish_ray(S, so, d, false, sh_rt[tid]);
+            sh_cnt0[r0.status][tid] += 1u;
+            if (r0.status == 0) {
+              sh_uv0[0][tid] += r0.u;
+              sh_uv0[1][tid] += r0.v;
+            }
+            r = finish_ray(S, so, d, true, sh_rt[tid]);
+          } else {
+            r.status = 1;
+            r.steps = 0;
+          }
+        } else {
+          r = trace_ray(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid]);
+        }
+      }
       if (k == 0 && S.accumulate) {  // block-uniform branch
         if (r.status == 0) {  // spot_pixel_window of the pilot, clipped to the frame
           const double cc = r.u / S.pitch + 0.5 * S.W;
@@ -306,6 +355,19 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
 #pragma unroll
       for (int j = 0; j < 7; ++j) sh_l[j][warp] = cnt[j];
     }
+    if (kPair) {
+      const double su0 = warp_sum(sh_uv0[0][tid]);
+      const double sv0 = warp_sum(sh_uv0[1][tid]);
+      unsigned long long c0[7];
+#pragma unroll
+      for (int j = 0; j < 7; ++j) c0[j] = warp_sum((unsigned long long)sh_cnt0[j][tid]);
+      if (lane == 0) {
+        sh_d0[0][warp] = su0;
+        sh_d0[1][warp] = sv0;
+#pragma unroll
+        for (int j = 0; j < 7; ++j) sh_l0[j][warp] = c0[j];
+      }
+    }
     __syncthreads();
     if (S.accumulate) {  // flush the tile (composite_tile, engine.cpp:181-187)
       const int tc0 = sh_tile[0], tr0 = sh_tile[1], tw = sh_tile[2], th = sh_tile[3];
@@ -333,6 +395,22 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
 #pragma unroll
       for (int j = 1; j < 7; ++j)
         if (l[j]) atomicAdd(&S.counters[j - 1], l[j]);
+      if (kPair) {
+        double a0 = 0.0, b0 = 0.0;
+        unsigned long long m[7] = {0, 0, 0, 0, 0, 0, 0};
+        for (int k = 0; k < kWarps; ++k) {
+          a0 += sh_d0[0][k];
+          b0 += sh_d0[1][k];
+#pragma unroll
+          for (int j = 0; j < 7; ++j) m[j] += sh_l0[j][k];
+        }
+        S.hit_sum0[2 * src] = a0;
+        S.hit_sum0[2 * src + 1] = b0;
+        S.landed0[src] = (long long)m[0];
+#pragma unroll
+        for (int j = 1; j < 6; ++j)
+          if (m[j]) atomicAdd(&S.counters0[j - 1], m[j]);
+      }
     }
     __syncthreads();
   }
@@ -426,16 +504,19 @@ __global__ void quantize_kernel(const double* __restrict__ img, int64_t n, doubl
 static size_t render_smem() { return (size_t)kTileCap * sizeof(uint32_t); }
 
 int render_occupancy(int* blocks_per_sm) {
-  cudaFuncSetAttribute(render_emitters, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(render_emitters<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)render_smem());
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, render_emitters,
+  cudaFuncSetAttribute(render_emitters<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)render_smem());
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, render_emitters<false>,
                                                             kBlock, render_smem());
 }
 
 cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream) {
-  cudaFuncSetAttribute(render_emitters, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)render_smem());
-  render_emitters<<<grid, kBlock, render_smem(), stream>>>(s);
+  if (s.pair)
+    render_emitters<true><<<grid, kBlock, render_smem(), stream>>>(s);
+  else
+    render_emitters<false><<<grid, kBlock, render_smem(), stream>>>(s);
   return cudaGetLastError();
 }
 

@@ -93,6 +93,12 @@ struct KScene {
   unsigned long long* counters;     // [0..4] lost, aperture, miss, tir, sensor_miss; [5] steps
   int* queue;                       // work counter
   int* err_flag;
+  // bos_run pair mode: also follow every emitted ray without the field and
+  // accumulate that leg's DotHitStats / counters here (no image)
+  int32_t pair, pad_pair;
+  double* hit_sum0;
+  long long* landed0;
+  unsigned long long* counters0;
 };
 
 // FP64 GriddedField nodes for the validation build (kernels_fp64.cu).

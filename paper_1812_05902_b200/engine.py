@@ -120,6 +120,26 @@ class GpuTracer:
         res.quantized = qimg
         return res
 
+    def trace_bos_pair(self, scene: FlatScene):
+        """rb_trace_bos_pair: bos_run's reference and gradient traces in one pass.
+        Returns (reference TraceResult, gradient TraceResult), stats only."""
+        s, keep = scene.to_c()
+        n = scene.n_sources
+        res = []
+        outs = []
+        for _ in range(2):
+            hit = np.zeros((n, 2))
+            landed = np.zeros(n, dtype=np.int64)
+            o = abi.TraceOut()
+            o.hit_sum = abi.dptr(hit) if n else None
+            o.landed = abi.i64ptr(landed) if n else None
+            res.append((hit, landed))
+            outs.append(o)
+        rc = self.lib.rb_trace_bos_pair(self.ctx, C.byref(s), C.byref(outs[0]), C.byref(outs[1]))
+        if rc:
+            _raise(self.lib, self.ctx, rc, "rb_trace_bos_pair")
+        return tuple(TraceResult(h, l, None, report_from(o)) for (h, l), o in zip(res, outs))
+
     def trace_debug(self, scene: FlatScene, source_index: int, ray_index: int,
                     max_records: int = 100000) -> np.ndarray:
         """rb_trace_debug: StepObserver records (xi, r, t) of one ray, shape (n, 7)."""

@@ -13,5 +13,4 @@ for i, l in enumerate(lines):
         if any('LDG.E.128' in x for x in region) and len(region) < 1200:
             sp = [x for x in region if 'STL' in x or 'LDL' in x]
             print(f"GRIN loop {hex(t)}-{hex(addr[i])}: {len(region)} instr, {len(sp)} spill instr")
-            break
 print("total spill instr", sum(1 for x in lines if 'STL' in x or 'LDL' in x))

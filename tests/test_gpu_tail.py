@@ -50,3 +50,24 @@ def test_device_quantize_matches_host_quantize(tracer, name, bits):
     # and within one count of quantizing the reference's own image
     ref_q = S.quantize(g["image_1"], bits, gain).astype(np.int64)
     assert np.abs(res.quantized.astype(np.int64) - ref_q).max() <= 1
+
+
+@pytest.mark.parametrize("name", ["small", "blob", "field3d", "shock_particles"])
+def test_bos_pair_equals_two_traces(tracer, name):
+    """f2: rb_trace_bos_pair == rb_trace(no field) + rb_trace(field), bit for bit,
+    and the per-dot displacement (measure_dot_displacements, bos.cpp:97-112)
+    matches the reference's within 1e-3 px."""
+    scene, field, g = load(name)
+    tracer.set_field(field)
+    ref_leg, grad_leg = tracer.trace_bos_pair(scene)
+    a = tracer.run_trace(scene, False, False)
+    b = tracer.run_trace(scene, True, False)
+    for x, y in ((ref_leg, a), (grad_leg, b)):
+        assert np.array_equal(x.hit_sum, y.hit_sum) and np.array_equal(x.landed, y.landed)
+        for k in ("emitted", "landed", "lost", "blocked_aperture", "blocked_miss", "blocked_tir",
+                  "blocked_sensor_miss"):
+            assert x.report[k] == y.report[k], k
+    m = (ref_leg.landed > 0) & (grad_leg.landed > 0)
+    disp = grad_leg.hit_sum[m] / grad_leg.landed[m, None] - ref_leg.hit_sum[m] / ref_leg.landed[m, None]
+    disp_ref = g["hit_sum_1"][m] / g["landed_1"][m, None] - g["hit_sum_0"][m] / g["landed_0"][m, None]
+    assert np.abs(disp - disp_ref).max() / scene.sensor.pitch < 1e-3
