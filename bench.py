@@ -283,6 +283,7 @@ def main_ours(args, rank, world, local):
 
     def step():
         img.zero_()
+        torch.cuda.current_stream().synchronize()   # the library runs on its own stream
         rep = tracer.trace_shard(scene, True, True, rank, world, img.data_ptr())
         if world > 1:
             dist.reduce(img, 0)
@@ -330,6 +331,7 @@ def main_ours(args, rank, world, local):
                 tracer.run_trace(scene, True, True)
             else:
                 img.zero_()
+                torch.cuda.current_stream().synchronize()
                 tracer.trace_shard(scene, True, True, rank, world, img.data_ptr())
                 dist.reduce(img, 0)
                 if rank == 0:

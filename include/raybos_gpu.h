@@ -217,7 +217,10 @@ int rb_plan_shards(const rb_scene* scene, int64_t shard_count, int32_t* shard_of
  * traces the sources rb_plan_shards assigns to shard_index, on device 0 of the
  * context.  image_fixed, if non-NULL, is a DEVICE pointer to W*H uint64 that
  * the partial fixed-point image (radiance * 2^31) is added into; the caller
- * reduces those buffers across ranks (one NCCL sum).  Stats are written only
+ * reduces those buffers across ranks (one NCCL sum).  The library's stream first
+ * waits for work already queued on the device's legacy default stream (e.g. the
+ * caller zeroing the buffer); work on other caller streams must be synchronized
+ * by the caller.  The call returns after the image is complete.  Stats are written only
  * for the owned sources; counters cover only the owned sources.  out->image is
  * ignored. */
 int rb_trace_shard(rb_ctx* ctx, const rb_scene* scene, int with_field, int accumulate_image,

@@ -59,6 +59,7 @@ struct Device {
   int blocks_per_sm = 1;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_join = nullptr;  // orders our stream after the legacy default stream
   float4* grid = nullptr;
   size_t grid_bytes = 0;
   Buf sources, ids, order, image, hit, landed, counters, queue, err, dimage, rays_src, rays_idx,
@@ -325,6 +326,16 @@ struct PartialOut {
 
 // One device renders the given work list into dev.image (already zeroed or
 // caller-owned when image_override != nullptr).
+// Caller-provided device buffers (rb_trace_shard's image, rb_image_from_fixed's
+// input) are typically written on the caller's stream, usually the device's
+// legacy default stream (torch's default).  Our stream is non-blocking, so make
+// it wait for everything already queued there before touching them.
+cudaError_t join_default_stream(Device& dev) {
+  cudaError_t e = cudaEventRecord(dev.ev_join, 0);
+  if (e != cudaSuccess) return e;
+  return cudaStreamWaitEvent(dev.stream, dev.ev_join, 0);
+}
+
 int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& base,
               const std::vector<int32_t>& work, unsigned long long* image_target,
               PartialOut& po) {
@@ -333,6 +344,7 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   const size_t npx = static_cast<size_t>(s->sensor.width_px) * s->sensor.height_px;
   cudaStream_t st = dev.stream;
   rbk::KScene k = base;
+  if (image_target) RB_CUDA(ctx, join_default_stream(dev));
   RB_CUDA(ctx, dev.sources.ensure(sizeof(double) * 3 * n));
   RB_CUDA(ctx, cudaMemcpyAsync(dev.sources.p, s->sources, sizeof(double) * 3 * n,
                                cudaMemcpyHostToDevice, st));
@@ -521,7 +533,8 @@ int rb_create(int n_devices, int first_device, rb_ctx** out, char* err, size_t e
     cudaSetDevice(dev.ordinal);
     dev.sms = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&dev.stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreate(&dev.ev0) != cudaSuccess || cudaEventCreate(&dev.ev1) != cudaSuccess) {
+        cudaEventCreate(&dev.ev0) != cudaSuccess || cudaEventCreate(&dev.ev1) != cudaSuccess ||
+        cudaEventCreateWithFlags(&dev.ev_join, cudaEventDisableTiming) != cudaSuccess) {
       delete ctx;
       return fail(nullptr, RB_E_CUDA, "rb_create: stream/event creation failed", err, errlen);
     }
@@ -562,6 +575,7 @@ void rb_destroy(rb_ctx* ctx) {
       b->release();
     if (d.ev0) cudaEventDestroy(d.ev0);
     if (d.ev1) cudaEventDestroy(d.ev1);
+    if (d.ev_join) cudaEventDestroy(d.ev_join);
     if (d.stream) cudaStreamDestroy(d.stream);
   }
   delete ctx;
@@ -825,6 +839,7 @@ int rb_image_from_fixed(rb_ctx* ctx, const uint64_t* image_fixed_device, int64_t
   Device& d0 = ctx->devs[0];
   RB_CUDA(ctx, cudaSetDevice(d0.ordinal));
   RB_CUDA(ctx, d0.dimage.ensure(static_cast<size_t>(n_pixels) * sizeof(double)));
+  RB_CUDA(ctx, join_default_stream(d0));
   RB_CUDA(ctx, rbk::launch_image_finalize(reinterpret_cast<const unsigned long long*>(image_fixed_device),
                                           d0.dimage.as<double>(), n_pixels, d0.stream));
   RB_CUDA(ctx, cudaMemcpyAsync(image_host, d0.dimage.p, static_cast<size_t>(n_pixels) * sizeof(double),

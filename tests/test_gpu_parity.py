@@ -82,6 +82,7 @@ def test_shards_are_bit_identical_to_single_run(tracer, name):
     full = tracer.run_trace(scene, True, True)
     for count in (1, 2, 3, 8):
         buf = torch.zeros(scene.height * scene.width, dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
         hit = np.zeros((scene.n_sources, 2))
         landed = np.zeros(scene.n_sources, dtype=np.int64)
         tot = 0
