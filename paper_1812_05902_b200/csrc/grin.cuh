@@ -288,6 +288,11 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
   cache.key = ~0u;
 #endif
   const int max_steps = S.max_steps;
+#ifndef RB_STEP_UNROLL
+#define RB_STEP_UNROLL 1
+#endif
+  constexpr int kStepUnroll = RB_STEP_UNROLL;
+#pragma unroll kStepUnroll
   for (int step = 0; step < max_steps; ++step) {
     const float fs = (float)step;
     const float pbx = fmaf(ax, fs + 0.5f, q0x), pby = fmaf(ay, fs + 0.5f, q0y),

@@ -11,7 +11,9 @@ fp64 = os.path.join(PKG, "_build", "kernels_fp64.cu.o")
 variants = []
 for v in sys.argv[1:] or ["256x2c1", "256x3c0"]:
     b, rest = v.split("x")
-    u, dd, sp = 1, 1, 1
+    u, dd, sp, ur = 1, 1, 0, 1
+    if "r" in rest:
+        rest, ur = rest.split("r")
     if "s" in rest:
         rest, sp = rest.split("s")
     if "d" in rest:
@@ -19,12 +21,12 @@ for v in sys.argv[1:] or ["256x2c1", "256x3c0"]:
     if "u" in rest:
         rest, u = rest.split("u")
     m, c = rest.split("c") if "c" in rest else (rest, "1")
-    variants.append((int(b), int(m), int(c), int(u), int(dd), int(sp)))
-for blk, mb, cc, uu, dd, sp in variants:
-    obj = os.path.join(OUT, f"k_{blk}_{mb}_c{cc}_u{uu}_d{dd}_s{sp}.o")
+    variants.append((int(b), int(m), int(c), int(u), int(dd), int(sp), int(ur)))
+for blk, mb, cc, uu, dd, sp, ur in variants:
+    obj = os.path.join(OUT, f"k_{blk}_{mb}_c{cc}_u{uu}_d{dd}_s{sp}_r{ur}.o")
     subprocess.run([NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", *ARCH,
-                    f"-DRB_BLOCK={blk}", f"-DRB_MINB={mb}", f"-DRB_CELL_CACHE={cc}", f"-DRB_UNIFORM_RELOAD={uu}", f"-DRB_DITHER={dd}", f"-DRB_SPECULATE={sp}", f"-I{ROOT}/include", "-c",
+                    f"-DRB_BLOCK={blk}", f"-DRB_MINB={mb}", f"-DRB_CELL_CACHE={cc}", f"-DRB_UNIFORM_RELOAD={uu}", f"-DRB_DITHER={dd}", f"-DRB_SPECULATE={sp}", f"-DRB_STEP_UNROLL={ur}", f"-I{ROOT}/include", "-c",
                     os.path.join(PKG, "csrc", "kernels.cu"), "-o", obj], check=True)
-    lib = os.path.join(OUT, f"libraybos_gpu_{blk}_{mb}_c{cc}_u{uu}_d{dd}_s{sp}.so")
+    lib = os.path.join(OUT, f"libraybos_gpu_{blk}_{mb}_c{cc}_u{uu}_d{dd}_s{sp}_r{ur}.so")
     subprocess.run([NVCC, "-shared", *ARCH, capi, fp64, obj, "-o", lib, "-ldl", "-lpthread"], check=True)
     print(lib)
