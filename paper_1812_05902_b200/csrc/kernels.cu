@@ -145,6 +145,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
     }
     const float mass_u = 0.5f * (e - eu0);
     const float scale = energy_fx / (mass_u * mass_v);
+    const bool cols_in_tile = c0 >= tc0 && c1 < tc0 + tw;
     // Rows are visited starting at a lane-dependent row (wrapping once), so the
     // lanes of a coherent warp, whose spots coincide, add to different rows at
     // the same time instead of serialising on the same shared-memory words.
@@ -159,12 +160,26 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
       const float er1 = r == r1 ? ev1 : erff(erf_arg(S, r + 1, rc));
       const float row_w = 0.5f * (er1 - er) * scale;
       er = er1;
+      // Fast path when every active lane's current row lies in the shared tile
+      // (which lies in the frame): no per-pixel bounds checks.  The choice is
+      // warp-uniform, so the warp never executes both loops for one row.
+      if (__all_sync(__activemask(), cols_in_tile && (unsigned)(r - tr0) < (unsigned)th)) {
+        uint32_t* trow = tile + (r - tr0) * tw + (c0 - tc0);
 #pragma unroll
-      for (int k = 0; k < kMaxSpot; ++k) {
-        const int c = c0 + k;
-        if (k < ncol && c >= 0 && c < S.W) {
-          const uint32_t f = dround(wu[k] * row_w, w);
-          if (f) add_px(S, tile, tc0, tr0, tw, th, c, r, f);
+        for (int k = 0; k < kMaxSpot; ++k) {
+          if (k < ncol) {
+            const uint32_t f = dround(wu[k] * row_w, w);
+            if (f) atomicAdd(trow + k, f);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kMaxSpot; ++k) {
+          const int c = c0 + k;
+          if (k < ncol && c >= 0 && c < S.W) {
+            const uint32_t f = dround(wu[k] * row_w, w);
+            if (f) add_px(S, tile, tc0, tr0, tw, th, c, r, f);
+          }
         }
       }
     }

@@ -18,7 +18,10 @@ constexpr int kMaxElements = 8;
 constexpr int kBlock = RB_BLOCK;     // threads per CTA (one emitter at a time)
 constexpr int kMinBlocks = RB_MINB;  // resident CTAs per SM the register budget targets
 constexpr int kTileCap = 6144;       // u32 entries of the per-emitter shared tile (24 KB)
-constexpr int kMaxSpot = 16;         // register fast path: spot windows up to 16 columns
+#ifndef RB_MAX_SPOT
+#define RB_MAX_SPOT 12  // 16 measured 10-40% slower (code size); bench spots are <= 11 wide
+#endif
+constexpr int kMaxSpot = RB_MAX_SPOT;  // register fast path: spot windows up to this many columns
 
 // raybos::SphericalSurface with the derived quantities intersect_sphere
 // recomputes on every call (optics.cpp:34-57) hoisted to the host.
