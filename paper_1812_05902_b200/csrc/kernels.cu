@@ -96,12 +96,17 @@ __device__ __forceinline__ float erf_arg(const KScene& S, int pix, double center
 }
 
 // Unbiased deterministic rounding of a fixed-point contribution: floor(x + u)
-// with one dither offset u in [0, 1) per ray, drawn from the ray's counter-RNG
-// key.  Over the rays that hit a pixel the u are independent and uniform, so
-// E[f] = x and the rounding errors of coherent rays (which all see nearly the
-// same weights) do not accumulate into a bias (round-to-nearest left 5e-5
-// relative L2 on 1e4-ray bundles; this leaves < 1e-6).  u depends only on the
-// ray, never on scheduling, so images stay bit-reproducible.
+// with a dither offset u in [0, 1) per (ray, spot row): a Weyl step of the
+// ray's counter-RNG key by the absolute row index.  Over the rays that hit a
+// pixel the u are independent and uniform, so E[f] = x and the rounding errors
+// of coherent rays (which all see nearly the same weights) do not accumulate
+// into a bias (round-to-nearest left 5e-5 relative L2 on 1e4-ray bundles; this
+// leaves < 1e-6); a fresh u per row keeps one ray's rounding errors from all
+// moving together.  u depends only on the ray and the pixel row, never on
+// scheduling, so images stay bit-reproducible.
+__device__ __forceinline__ float row_dither(uint32_t seed, int row) {
+  return __uint_as_float(0x3f800000u | ((seed + (uint32_t)row * 0x9E3779B9u) >> 9)) - 1.0f;
+}
 #ifndef RB_DITHER
 #define RB_DITHER 1
 #endif
@@ -113,14 +118,13 @@ __device__ __forceinline__ uint32_t dround(float x, float u) {
 // normalized over the full window, in-frame pixels only.
 __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uint32_t* tile, int tc0,
                                      int tr0, int tw, int th, uint32_t seed) {
-  const float w = __uint_as_float(0x3f800000u | (seed >> 9)) - 1.0f;  // dither in [0, 1)
   const double cc = u / S.pitch + 0.5 * S.W;
   const double rc = 0.5 * S.H - v / S.pitch;
   const float energy_fx = (float)(S.radiance * 2147483648.0);
   if (S.degenerate) {  // sensor.cpp:71-77
     const int col = (int)floor(cc), row = (int)floor(rc);
     if (col >= 0 && col < S.W && row >= 0 && row < S.H)
-      add_px(S, tile, tc0, tr0, tw, th, col, row, dround(energy_fx, w));
+      add_px(S, tile, tc0, tr0, tw, th, col, row, dround(energy_fx, row_dither(seed, row)));
     return;
   }
   const int c0 = (int)floor(cc - S.half_width), c1 = (int)floor(cc + S.half_width);
@@ -159,6 +163,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
       }
       const float er1 = r == r1 ? ev1 : erff(erf_arg(S, r + 1, rc));
       const float row_w = 0.5f * (er1 - er) * scale;
+      const float w = row_dither(seed, r);
       er = er1;
       // Fast path when every active lane's current row lies in the shared tile
       // (which lies in the frame): no per-pixel bounds checks.  The choice is
@@ -191,6 +196,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
     for (int r = rb; r <= re; ++r) {
       const float er1 = r == r1 ? ev1 : erff(erf_arg(S, r + 1, rc));
       const float row_w = 0.5f * (er1 - er) * scale;
+      const float w = row_dither(seed, r);
       er = er1;
       float ec = cb == c0 ? eu0 : erff(erf_arg(S, cb, cc));
       for (int c = cb; c <= ce; ++c) {
@@ -235,7 +241,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
   // memory, not registers: they change once per ray, and keeping them out of
   // the register file during the RK4 loop is what lets K1 fit its budget.
   __shared__ double sh_uv[2][kBlock];
-  __shared__ unsigned sh_cnt[7][kBlock];     // landed, lost, aperture, miss, tir, smiss, steps
+  __shared__ unsigned sh_cnt[6][kBlock];     // landed, lost, aperture, miss, tir, smiss
+  __shared__ unsigned long long sh_steps[kBlock];  // RK4 steps (64-bit: rays x max_steps)
   __shared__ double sh_rt[kBlock][7];        // R0, T0 of the ray in flight (grin.cuh)
   __shared__ double sh_d[2][kWarps];
   __shared__ unsigned long long sh_l[7][kWarps];
@@ -270,7 +277,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
     sh_uv[0][tid] = sh_uv[1][tid] = 0.0;
     sh_uv0[0][tid] = sh_uv0[1][tid] = 0.0;
 #pragma unroll
-    for (int j = 0; j < 7; ++j) sh_cnt[j][tid] = sh_cnt0[j][tid] = 0u;
+    for (int j = 0; j < 6; ++j) sh_cnt[j][tid] = 0u;
+#pragma unroll
+    for (int j = 0; j < 7; ++j) sh_cnt0[j][tid] = 0u;
+    sh_steps[tid] = 0ull;
     __syncthreads();
     if (sh_work >= S.n_work) break;
 
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
         __syncthreads();
       }
       if (r.status >= 0) {
-        sh_cnt[6][tid] += (unsigned)r.steps;
+        sh_steps[tid] += (unsigned long long)r.steps;
         sh_cnt[r.status][tid] += 1u;
         if (r.status == 0) {
           sh_uv[0][tid] += r.u;
@@ -363,7 +373,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
     double sv = warp_sum(sh_uv[1][tid]);
     unsigned long long cnt[7];
 #pragma unroll
-    for (int j = 0; j < 7; ++j) cnt[j] = warp_sum((unsigned long long)sh_cnt[j][tid]);
+    for (int j = 0; j < 6; ++j) cnt[j] = warp_sum((unsigned long long)sh_cnt[j][tid]);
+    cnt[6] = warp_sum(sh_steps[tid]);
     if (lane == 0) {
       sh_d[0][warp] = su;
       sh_d[1][warp] = sv;

@@ -177,3 +177,22 @@ def test_cpp_dropin_adapter_matches_reference():
     bad = [l for l in lines if l.get("ok") is False]
     assert r.returncode == 0 and not bad, (bad, r.stderr[-2000:])
     assert sum(1 for l in lines if "check" in l) >= 9
+
+
+@pytest.mark.parametrize("dtau_scale,window", [(3.0, 4.0), (1.0, 9.0), (1e-4, 4.0)])
+def test_wide_and_degenerate_spots_match_oracle(tracer, oracle, dtau_scale, window):
+    """accumulate_spot's other regimes (sensor.cpp:57-122): windows wider than the
+    register fast path (> 12 columns) and the degenerate single-pixel spot
+    (sigma < 1e-3 pitch), checked live against the bit-exact oracle."""
+    from paper_1812_05902_b200 import abi
+    scene, field, g = load("blob")
+    scene.d_tau *= dtau_scale
+    scene.sensor = abi.Sensor.from_buffer_copy(scene.sensor)
+    scene.sensor.window_sigmas = window
+    tracer.set_field(field)
+    a = tracer.run_trace(scene, True, True)
+    b = oracle.trace(scene, field, True, True)
+    assert np.array_equal(a.landed, b.landed)
+    assert rel_l2(a.image, b.image) < IMG_RTOL
+    # energy: the dithered fixed point is unbiased; its noise stays ~1e-6
+    assert abs(a.image.sum() - b.image.sum()) / b.image.sum() < 2e-6
