@@ -194,7 +194,8 @@ int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, 
 int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rho,
                          double gladstone_dale_k);
 int rb_clear_field(rb_ctx* ctx);
-/* Bytes of device memory held by the packed grid on each device. */
+/* Bytes of device memory held by the packed grid (and its per-cell coefficient
+ * table, when one was built) on each device. */
 int64_t rb_field_bytes(const rb_ctx* ctx);
 
 /* ---- the hot path -------------------------------------------------------- */

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -62,6 +63,8 @@ struct Device {
   cudaEvent_t ev_join = nullptr;  // orders our stream after the legacy default stream
   float4* grid = nullptr;
   size_t grid_bytes = 0;
+  rbk::CellCoef* cells = nullptr;  // per-cell coefficient table (optional, 8x the grid)
+  size_t cells_bytes = 0;
   Buf sources, ids, order, image, hit, landed, counters, queue, err, dimage, rays_src, rays_idx,
       rays_uv, rays_status, rays_steps;
   Buf f64[4];  // FP64 node copy (n, gx, gy, gz) for the validation build
@@ -227,6 +230,8 @@ rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, in
     k.g_mx = static_cast<float>(k.nx - 1);
     k.g_my = static_cast<float>(k.ny - 1);
     k.g_mz = static_cast<float>(k.nz - 1);
+    k.c_nx = static_cast<unsigned>(k.nx - 1);
+    k.c_nxny = static_cast<unsigned>(k.nx - 1) * static_cast<unsigned>(k.ny - 1);
     const double h = s->delta_xi;
     const double hs[3] = {h / k.spacing.x, h / k.spacing.y, h / k.spacing.z};
     float* dst[6][3] = {{&k.hx, &k.hy, &k.hz},    {&k.hhx, &k.hhy, &k.hhz},
@@ -383,6 +388,7 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   k.queue = dev.queue.as<int>();
   k.err_flag = dev.queue.as<int>() + 1;
   k.grid = dev.grid;
+  k.cell_table = dev.cells;
   if (k.accumulate) {
     if (image_target) {
       k.image = image_target;
@@ -439,17 +445,48 @@ void fill_report(rb_trace_out* out, const rb_scene* s, int64_t owned_sources,
   out->config_hash = s->config_hash;
 }
 
-int upload_grid(rb_ctx* ctx, Device& dev, size_t count) {
-  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+void free_field(Device& dev) {
+  cudaSetDevice(dev.ordinal);
   if (dev.grid) cudaFree(dev.grid);
+  if (dev.cells) cudaFree(dev.cells);
   dev.grid = nullptr;
   dev.grid_bytes = 0;
+  dev.cells = nullptr;
+  dev.cells_bytes = 0;
+}
+
+int upload_grid(rb_ctx* ctx, Device& dev, size_t count) {
+  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+  free_field(dev);
   RB_CUDA(ctx, cudaMalloc(&dev.grid, count * sizeof(float4)));
   dev.grid_bytes = count * sizeof(float4);
   return RB_OK;
 }
 
-// Keeps the grid hot in L2 with an access-policy window on the render stream.
+// Per-cell coefficient table (kernels.h CellCoef): a reload in the RK4 loop
+// then reads one 128 B line instead of 8 corners + 28 FADDs.  Built when it
+// fits in half the free device memory; RAYBOS_CELL_TABLE=0 turns it off.
+// Results are bit-identical either way.
+int build_cell_table(rb_ctx* ctx, Device& dev, const rb_field_desc* desc) {
+  const char* env = std::getenv("RAYBOS_CELL_TABLE");
+  if (env && env[0] == '0') return RB_OK;
+  const size_t cells = static_cast<size_t>(desc->nx - 1) * (desc->ny - 1) * (desc->nz - 1);
+  const size_t bytes = cells * sizeof(rbk::CellCoef);
+  size_t free_b = 0, total_b = 0;
+  RB_CUDA(ctx, cudaMemGetInfo(&free_b, &total_b));
+  if (bytes > free_b / 2) return RB_OK;
+  if (cudaMalloc(&dev.cells, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    dev.cells = nullptr;
+    return RB_OK;
+  }
+  dev.cells_bytes = bytes;
+  RB_CUDA(ctx, rbk::launch_build_cells(dev.grid, desc->nx, desc->ny, desc->nz, dev.cells,
+                                       dev.stream));
+  return RB_OK;
+}
+
+// Keeps the field hot in L2 with an access-policy window on the render stream.
 void set_l2_window(Device& dev) {
   cudaSetDevice(dev.ordinal);
   int max_persist = 0, max_window = 0;
@@ -458,8 +495,10 @@ void set_l2_window(Device& dev) {
   if (max_persist <= 0 || max_window <= 0 || !dev.grid) return;
   cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(max_persist));
   cudaStreamAttrValue attr{};
-  const size_t win = std::min<size_t>(dev.grid_bytes, static_cast<size_t>(max_window));
-  attr.accessPolicyWindow.base_ptr = dev.grid;
+  void* base = dev.cells ? static_cast<void*>(dev.cells) : static_cast<void*>(dev.grid);
+  const size_t bytes = dev.cells ? dev.cells_bytes : dev.grid_bytes;
+  const size_t win = std::min<size_t>(bytes, static_cast<size_t>(max_window));
+  attr.accessPolicyWindow.base_ptr = base;
   attr.accessPolicyWindow.num_bytes = win;
   attr.accessPolicyWindow.hitRatio =
       std::min(1.0f, static_cast<float>(max_persist) / static_cast<float>(win));
@@ -565,8 +604,7 @@ void rb_destroy(rb_ctx* ctx) {
   for (ncclComm_t c : ctx->comms)
     if (c && ctx->nccl.destroy) ctx->nccl.destroy(c);
   for (Device& d : ctx->devs) {
-    cudaSetDevice(d.ordinal);
-    if (d.grid) cudaFree(d.grid);
+    free_field(d);
     for (Buf& b : d.f64) b.release();
     for (Buf* b : {&d.qimage, &d.dbg, &d.dbg_n, &d.hit0, &d.landed0, &d.counters0}) b->release();
     for (Buf* b : {&d.sources, &d.ids, &d.order, &d.image, &d.hit, &d.landed, &d.counters,
@@ -602,6 +640,7 @@ int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, 
       RB_CUDA(ctx, rbk::launch_pack_nodes(st, st + chunk, st + 2 * chunk, st + 3 * chunk,
                                           dev.grid + off, static_cast<int64_t>(m), dev.stream));
     }
+    if (int rc = build_cell_table(ctx, dev, desc)) return rc;
     for (Buf& b : dev.f64) b.release();
     if (static_cast<long long>(count) <= RB_FP64_MAX_NODES) {
       const double* src[4] = {n, gx, gy, gz};
@@ -639,6 +678,7 @@ int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rh
     RB_CUDA(ctx, rbk::launch_build_from_density(drho.as<float>(), desc->nx, desc->ny, desc->nz,
                                                 gladstone_dale_k, d3(desc->spacing), dev.grid, 0,
                                                 desc->nz, dev.stream));
+    if (int rc = build_cell_table(ctx, dev, desc)) return rc;
     for (Buf& b : dev.f64) b.release();
     if (static_cast<long long>(count) <= RB_FP64_MAX_NODES) {
       for (Buf& b : dev.f64) RB_CUDA(ctx, b.ensure(count * sizeof(double)));
@@ -657,12 +697,7 @@ int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rh
 
 int rb_clear_field(rb_ctx* ctx) {
   if (!ctx) return RB_E_INVALID;
-  for (Device& dev : ctx->devs) {
-    cudaSetDevice(dev.ordinal);
-    if (dev.grid) cudaFree(dev.grid);
-    dev.grid = nullptr;
-    dev.grid_bytes = 0;
-  }
+  for (Device& dev : ctx->devs) free_field(dev);
   for (Device& dev : ctx->devs) {
     cudaSetDevice(dev.ordinal);
     for (Buf& b : dev.f64) b.release();
@@ -673,7 +708,9 @@ int rb_clear_field(rb_ctx* ctx) {
 }
 
 int64_t rb_field_bytes(const rb_ctx* ctx) {
-  return (ctx && !ctx->devs.empty()) ? static_cast<int64_t>(ctx->devs[0].grid_bytes) : 0;
+  return (ctx && !ctx->devs.empty())
+             ? static_cast<int64_t>(ctx->devs[0].grid_bytes + ctx->devs[0].cells_bytes)
+             : 0;
 }
 
 int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_image,
@@ -874,6 +911,7 @@ int rb_trace_rays(rb_ctx* ctx, const rb_scene* s, int with_field, int64_t n_rays
     k.source_ids = dev.ids.as<int64_t>();
   }
   k.grid = dev.grid;
+  k.cell_table = dev.cells;
   RB_CUDA(ctx, dev.queue.ensure(sizeof(int) * 2));
   RB_CUDA(ctx, cudaMemsetAsync(dev.queue.p, 0, sizeof(int) * 2, st));
   k.err_flag = dev.queue.as<int>() + 1;

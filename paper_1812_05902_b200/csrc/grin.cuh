@@ -113,6 +113,28 @@ __device__ __forceinline__ float4 f4sub(float4 p, float4 q) {
   return make_float4(p.x - q.x, p.y - q.y, p.z - q.z, p.w - q.w);
 }
 
+// Corner values -> polynomial coefficients (shared by the in-loop reload and
+// the table build so both give the same bits).
+__device__ __forceinline__ void cell_coefficients(float4 c000, float4 c100, float4 c010,
+                                                  float4 c110, float4 c001, float4 c101,
+                                                  float4 c011, float4 c111, float4& a, float4& b,
+                                                  float4& c, float4& d, float4& e, float4& f,
+                                                  float4& g, float4& h) {
+  a = c000;
+  b = f4sub(c100, c000);
+  c = f4sub(c010, c000);
+  d = f4sub(c001, c000);
+  const float4 e0 = f4sub(c110, c010), f0 = f4sub(c101, c001), g0 = f4sub(c011, c001);
+  e = f4sub(e0, b);
+  f = f4sub(f0, b);
+  g = f4sub(g0, c);
+  h = f4sub(f4sub(f4sub(c111, c011), e0), f);  // (c111-c011) - (c110-c010) - (c101-c001) + b
+}
+
+// kCells: read the cell's coefficients from the precomputed table (one 128 B
+// line, computed by build_cells_kernel with exactly these FP32 subtractions, so
+// both forms are bit-identical) instead of deriving them from the 8 corners.
+template <bool kCells>
 __device__ __forceinline__ void poly_load(const GridView& G, CellPoly& P, float qx, float qy,
                                           float qz, float& fx, float& fy, float& fz) {
   const unsigned i = min(__float2uint_rz(qx), G.S.g_ix);
@@ -127,20 +149,25 @@ __device__ __forceinline__ void poly_load(const GridView& G, CellPoly& P, float 
   P.ox = ox;
   P.oy = oy;
   P.oz = oz;
+  if (kCells) {
+    const float4* c = G.S.cell_table[k * G.S.c_nxny + j * G.S.c_nx + i].c;
+    P.a = __ldg(c);
+    P.b = __ldg(c + 1);
+    P.c = __ldg(c + 2);
+    P.d = __ldg(c + 3);
+    P.e = __ldg(c + 4);
+    P.f = __ldg(c + 5);
+    P.g = __ldg(c + 6);
+    P.h = __ldg(c + 7);  // (LDG.256 pairs measured 2% slower)
+    return;
+  }
   const float4* p0 = G.S.grid + (k * G.S.g_nxny + j * G.S.g_nx + i);
   const float4* p1 = p0 + G.S.g_nxny;
   const float4 c000 = __ldg(p0), c100 = __ldg(p0 + 1), c010 = __ldg(p0 + G.S.g_nx),
                c110 = __ldg(p0 + G.S.g_nx + 1), c001 = __ldg(p1), c101 = __ldg(p1 + 1),
                c011 = __ldg(p1 + G.S.g_nx), c111 = __ldg(p1 + G.S.g_nx + 1);
-  P.a = c000;
-  P.b = f4sub(c100, c000);
-  P.c = f4sub(c010, c000);
-  P.d = f4sub(c001, c000);
-  const float4 e0 = f4sub(c110, c010), f0 = f4sub(c101, c001), g0 = f4sub(c011, c001);
-  P.e = f4sub(e0, P.b);
-  P.f = f4sub(f0, P.b);
-  P.g = f4sub(g0, P.c);
-  P.h = f4sub(f4sub(f4sub(c111, c011), e0), P.f);  // (c111-c011) - (c110-c010) - (c101-c001) + b
+  cell_coefficients(c000, c100, c010, c110, c001, c101, c011, c111, P.a, P.b, P.c, P.d, P.e, P.f,
+                    P.g, P.h);
 }
 
 __device__ __forceinline__ float3 poly_eval(const CellPoly& P, float fx, float fy, float fz) {
@@ -156,6 +183,7 @@ __device__ __forceinline__ float3 poly_eval(const CellPoly& P, float fx, float f
 #define RB_SPECULATE 0  // measured 7% slower on tomo (duplicated Horner on reloads)
 #endif
 
+template <bool kCells>
 __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, float qx, float qy,
                                                 float qz) {
   float fx = qx - P.ox, fy = qy - P.oy, fz = qz - P.oz;
@@ -176,12 +204,12 @@ __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, 
 #endif
 #if RB_SPECULATE
   if (reload) {
-    poly_load(G, P, qx, qy, qz, fx, fy, fz);
+    poly_load<kCells>(G, P, qx, qy, qz, fx, fy, fz);
     D = poly_eval(P, fx, fy, fz);
   }
   return D;
 #else
-  if (reload) poly_load(G, P, qx, qy, qz, fx, fy, fz);
+  if (reload) poly_load<kCells>(G, P, qx, qy, qz, fx, fy, fz);
   return poly_eval(P, fx, fy, fz);
 #endif
 }
@@ -193,7 +221,7 @@ __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, 
 #define RB_CELL_CACHE 2
 #endif
 #if RB_CELL_CACHE == 2
-#define RB_SAMPLE_D(qx, qy, qz) sample_d_poly(G, cache, qx, qy, qz)
+#define RB_SAMPLE_D(qx, qy, qz) sample_d_poly<kCells>(G, cache, qx, qy, qz)
 #elif RB_CELL_CACHE == 1
 #define RB_SAMPLE_D(qx, qy, qz) sample_d_cached(G, cache, qx, qy, qz)
 #else
@@ -250,6 +278,7 @@ __device__ __forceinline__ bool aabb_intersect(const KScene& S, double3 o, doubl
 // Returns kMissed / kTraced / kLost / kInvalid; on kTraced (o, d) is the exit ray.
 // scratch: 7 doubles of shared memory for this thread; R0 and T0 are parked
 // there during the RK4 loop (they are only needed again at the exit).
+template <bool kCells>
 __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& d, int& steps,
                                           double* scratch) {
   steps = 0;

@@ -42,13 +42,14 @@ __device__ __forceinline__ bool emit_ray(const KScene& S, uint64_t ekey, double3
 }
 
 // Stages 2-4 of process_source (engine.cpp:112-137) for an emitted ray.
+template <bool kCells>
 __device__ __forceinline__ RayResult finish_ray(const KScene& S, double3 o, double3 d, bool field,
                                                 double* scratch) {
   RayResult r;
   r.steps = 0;
   r.u = r.v = 0.0;
   if (field) {
-    const int st = grin_trace(S, o, d, r.steps, scratch);
+    const int st = grin_trace<kCells>(S, o, d, r.steps, scratch);
     if (st == kLost || st == kInvalid) {
       r.status = 1;  // RB_RAY_LOST
       return r;
@@ -68,6 +69,7 @@ __device__ __forceinline__ RayResult finish_ray(const KScene& S, double3 o, doub
 }
 
 // process_source's per-ray body, engine.cpp:112-137.
+template <bool kCells>
 __device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, double3 src, int i,
                                                double* scratch) {
   double3 d;
@@ -78,7 +80,7 @@ __device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, d
     r.status = 1;
     return r;
   }
-  return finish_ray(S, src, d, S.with_field, scratch);
+  return finish_ray<kCells>(S, src, d, S.with_field, scratch);
 }
 
 // Tile-or-global fixed-point add of one pixel contribution.
@@ -228,7 +230,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 // whole pupil lattice).  Deposits outside the tile go straight to global.
 // kPair: bos_run pair mode (rb_trace_bos_pair), a separate instantiation so the
 // default kernel carries none of its code or registers.
-template <bool kPair>
+// kCells: the field is read through the per-cell coefficient table.
+template <bool kPair, bool kCells>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __grid_constant__ KScene S) {
   extern __shared__ uint32_t tile[];
   constexpr int kWarps = kBlock / 32;
@@ -304,19 +307,19 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
           const double3 so = make_double3(vso[0], vso[1], vso[2]);
           double3 d;
           if (emit_ray(S, ekey, so, i, d)) {
-            const RayResult r0 = finish_ray(S, so, d, false, sh_rt[tid]);
+            const RayResult r0 = finish_ray<kCells>(S, so, d, false, sh_rt[tid]);
             sh_cnt0[r0.status][tid] += 1u;
             if (r0.status == 0) {
               sh_uv0[0][tid] += r0.u;
               sh_uv0[1][tid] += r0.v;
             }
-            r = finish_ray(S, so, d, true, sh_rt[tid]);
+            r = finish_ray<kCells>(S, so, d, true, sh_rt[tid]);
           } else {
             r.status = 1;
             r.steps = 0;
           }
         } else {
-          r = trace_ray(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid]);
+          r = trace_ray<kCells>(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid]);
         }
       }
       if (k == 0 && S.accumulate) {  // block-uniform branch
@@ -443,6 +446,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
 }
 
 // Per-ray replay (rb_trace_rays).
+template <bool kCells>
 __global__ void trace_rays_kernel(const __grid_constant__ KScene S, int64_t n,
                                   const int64_t* __restrict__ srcs, const int32_t* __restrict__ rays,
                                   double* uv, int32_t* status, int32_t* steps) {
@@ -452,7 +456,7 @@ __global__ void trace_rays_kernel(const __grid_constant__ KScene S, int64_t n,
   const int64_t src = srcs[q];
   const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
   const double3 so = make_double3(S.sources[3 * src], S.sources[3 * src + 1], S.sources[3 * src + 2]);
-  const RayResult r = trace_ray(S, mix_bits(S.key_seed + sid), so, rays[q], sh_rt[threadIdx.x]);
+  const RayResult r = trace_ray<kCells>(S, mix_bits(S.key_seed + sid), so, rays[q], sh_rt[threadIdx.x]);
   uv[2 * q] = r.status == 0 ? r.u : nan("");
   uv[2 * q + 1] = r.status == 0 ? r.v : nan("");
   status[q] = r.status;
@@ -507,6 +511,32 @@ __global__ void build_from_density_kernel(const float* __restrict__ rho, int nx,
   }
 }
 
+// Per-cell coefficient table (KScene::cell_table) from the packed nodes.
+__global__ void build_cells_kernel(const float4* __restrict__ grid, int nx, int ny, int nz,
+                                   CellCoef* __restrict__ cells) {
+  const int64_t cx = nx - 1, cxy = (int64_t)(nx - 1) * (ny - 1);
+  const int64_t count = cxy * (nz - 1);
+  const int64_t nxny = (int64_t)nx * ny;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t / cxy, rem = t - k * cxy, j = rem / cx, i = rem - j * cx;
+    const float4* p0 = grid + (k * nxny + j * nx + i);
+    const float4* p1 = p0 + nxny;
+    float4 a, b, c, d, e, f, g, h;
+    cell_coefficients(p0[0], p0[1], p0[nx], p0[nx + 1], p1[0], p1[1], p1[nx], p1[nx + 1], a, b, c,
+                      d, e, f, g, h);
+    float4* o = cells[t].c;
+    o[0] = a;
+    o[1] = b;
+    o[2] = c;
+    o[3] = d;
+    o[4] = e;
+    o[5] = f;
+    o[6] = g;
+    o[7] = h;
+  }
+}
+
 // ------------------------------------------------ K2: image finalize
 __global__ void image_finalize_kernel(const unsigned long long* __restrict__ fx,
                                       double* __restrict__ out, int64_t n) {
@@ -530,19 +560,28 @@ __global__ void quantize_kernel(const double* __restrict__ img, int64_t n, doubl
 static size_t render_smem() { return (size_t)kTileCap * sizeof(uint32_t); }
 
 int render_occupancy(int* blocks_per_sm) {
-  cudaFuncSetAttribute(render_emitters<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)render_smem());
-  cudaFuncSetAttribute(render_emitters<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)render_smem());
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, render_emitters<false>,
-                                                            kBlock, render_smem());
+  const int smem = (int)render_smem();
+  cudaFuncSetAttribute(render_emitters<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(render_emitters<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(render_emitters<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(render_emitters<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      blocks_per_sm, render_emitters<false, false>, kBlock, render_smem());
 }
 
 cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream) {
-  if (s.pair)
-    render_emitters<true><<<grid, kBlock, render_smem(), stream>>>(s);
-  else
-    render_emitters<false><<<grid, kBlock, render_smem(), stream>>>(s);
+  const bool cells = s.with_field && s.cell_table;
+  if (s.pair) {
+    if (cells)
+      render_emitters<true, true><<<grid, kBlock, render_smem(), stream>>>(s);
+    else
+      render_emitters<true, false><<<grid, kBlock, render_smem(), stream>>>(s);
+  } else {
+    if (cells)
+      render_emitters<false, true><<<grid, kBlock, render_smem(), stream>>>(s);
+    else
+      render_emitters<false, false><<<grid, kBlock, render_smem(), stream>>>(s);
+  }
   return cudaGetLastError();
 }
 
@@ -550,8 +589,17 @@ cudaError_t launch_trace_rays(const KScene& s, int64_t n, const int64_t* src, co
                               double* uv, int32_t* status, int32_t* steps, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   const int bs = 128;
-  trace_rays_kernel<<<(unsigned)((n + bs - 1) / bs), bs, 0, stream>>>(s, n, src, ray, uv, status,
-                                                                      steps);
+  const unsigned blocks = (unsigned)((n + bs - 1) / bs);
+  if (s.with_field && s.cell_table)
+    trace_rays_kernel<true><<<blocks, bs, 0, stream>>>(s, n, src, ray, uv, status, steps);
+  else
+    trace_rays_kernel<false><<<blocks, bs, 0, stream>>>(s, n, src, ray, uv, status, steps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_cells(const float4* grid, int nx, int ny, int nz, CellCoef* cells,
+                               cudaStream_t stream) {
+  build_cells_kernel<<<148 * 8, 256, 0, stream>>>(grid, nx, ny, nz, cells);
   return cudaGetLastError();
 }
 

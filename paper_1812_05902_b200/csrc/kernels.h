@@ -32,6 +32,13 @@ struct DSurface {
   int pad;
 };
 
+// One grid cell's trilinear interpolant in polynomial form (grin.cuh CellPoly):
+// coefficients a..h of a + b fx + c fy + d fz + e fx fy + f fx fz + g fy fz +
+// h fx fy fz for the four channels.  128 B = one L1/L2 line per cell.
+struct __align__(128) CellCoef {
+  float4 c[8];
+};
+
 struct DElement {
   int kind, pad;
   double3 center, axis;
@@ -67,6 +74,9 @@ struct KScene {
   int32_t pad_patch;
   // density grid (float4: n-1, dn/dx, dn/dy, dn/dz)
   const float4* grid;
+  // optional per-cell coefficient table (nullptr = derive from the nodes)
+  const CellCoef* cell_table;
+  unsigned c_nx, c_nxny;         // cell strides: nx - 1, (nx - 1) * (ny - 1)
   int32_t nx, ny, nz, max_steps;
   double3 origin, spacing, box_lo, box_hi;
   double h;
@@ -131,6 +141,8 @@ cudaError_t launch_pack_nodes(const double* n, const double* gx, const double* g
 cudaError_t launch_build_from_density(const float* rho, int nx, int ny, int nz, double k,
                                       double3 spacing, float4* out, int z0, int z1,
                                       cudaStream_t stream);
+cudaError_t launch_build_cells(const float4* grid, int nx, int ny, int nz, CellCoef* cells,
+                               cudaStream_t stream);
 cudaError_t launch_image_finalize(const unsigned long long* fixed, double* out, int64_t n,
                                   cudaStream_t stream);
 

@@ -71,3 +71,27 @@ def test_bos_pair_equals_two_traces(tracer, name):
     disp = grad_leg.hit_sum[m] / grad_leg.landed[m, None] - ref_leg.hit_sum[m] / ref_leg.landed[m, None]
     disp_ref = g["hit_sum_1"][m] / g["landed_1"][m, None] - g["hit_sum_0"][m] / g["landed_0"][m, None]
     assert np.abs(disp - disp_ref).max() / scene.sensor.pitch < 1e-3
+
+
+@pytest.mark.parametrize("name", ["blob", "field3d", "shock_particles", "uniform_random"])
+def test_cell_table_is_bit_identical(tracer, name, monkeypatch):
+    """The per-cell coefficient table (capi.cpp build_cell_table) and the
+    in-loop derivation from the nodes give the same bits: images, hits, steps,
+    and the per-ray replay."""
+    scene, field, g = load(name)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RAYBOS_CELL_TABLE", flag)
+        tracer.set_field(field)
+        nodes = tracer.field_bytes()
+        res = tracer.run_trace(scene, True, True)
+        src = np.repeat(np.arange(scene.n_sources), 3)
+        ray = np.tile([0, scene.rays_per_source // 2, scene.rays_per_source - 1], scene.n_sources)
+        out[flag] = (nodes, res, tracer.trace_rays(scene, src, ray))
+    (b1, r1, t1), (b0, r0, t0) = out["1"], out["0"]
+    assert b1 > b0  # the table was built (and only in the first pass)
+    assert np.array_equal(r1.image, r0.image)
+    assert np.array_equal(r1.hit_sum, r0.hit_sum) and np.array_equal(r1.landed, r0.landed)
+    assert r1.report["total_steps"] == r0.report["total_steps"]
+    for a, b in zip(t1, t0):
+        assert np.array_equal(np.asarray(a), np.asarray(b), equal_nan=True)
