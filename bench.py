@@ -367,8 +367,11 @@ def main_ours(args, rank, world, local):
                                "max of register/immediate operand forms",
                 "per_ray": f"{FLOPS_PER_STEP:.0f} flops/RK4 step + {FLOPS_PER_RAY:.0f}; "
                            f"{steps_sum / max(rays_local, 1):.1f} steps/ray measured",
-                "gather": {"achieved_gbs": gather, "l2_gather_peak_gbs": peaks["l2_gather_gbs"],
-                           "frac": gather / peaks["l2_gather_gbs"],
+                # what the samples would move if each gathered its 8 corners
+                # (3 x 8 x 16 B per step): above the measured L2 gather peak,
+                # which is why K1 caches the cell in registers instead
+                "gather": {"uncached_equivalent_gbs": gather,
+                           "l2_gather_peak_gbs": peaks["l2_gather_gbs"],
                            "bytes_per_step": GATHER_BYTES_PER_STEP},
                 "ffma_reg_tflops": peaks["ffma_reg_tflops"],
                 "ffma_imm_tflops": peaks["ffma_imm_tflops"], "hbm_gbs_measured": measured_hbm()}

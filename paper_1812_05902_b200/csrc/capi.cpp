@@ -389,6 +389,15 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   k.err_flag = dev.queue.as<int>() + 1;
   k.grid = dev.grid;
   k.cell_table = dev.cells;
+  if (k.with_field && dev.cells) {
+    // L2 prefetch on reloads pays when the cones' cells do not stay L2
+    // resident (measured: bos 256^3 +3%, 1024^3 +2.5%, tomo 256x256x128 -3%);
+    // RAYBOS_PREFETCH=0/1 overrides the size rule.
+    const char* pf = std::getenv("RAYBOS_PREFETCH");
+    k.prefetch = pf ? (pf[0] != '0') : (dev.cells_bytes > (size_t(3) << 29));
+    const double fine = std::min(k.spacing.x, std::min(k.spacing.y, k.spacing.z));
+    k.prefetch_steps = static_cast<float>(fine / k.h);
+  }
   if (k.accumulate) {
     if (image_target) {
       k.image = image_target;
@@ -464,9 +473,10 @@ int upload_grid(rb_ctx* ctx, Device& dev, size_t count) {
 }
 
 // Per-cell coefficient table (kernels.h CellCoef): a reload in the RK4 loop
-// then reads one 128 B line instead of 8 corners + 28 FADDs.  Built when it
-// fits in half the free device memory; RAYBOS_CELL_TABLE=0 turns it off.
-// Results are bit-identical either way.
+// then reads one 128 B line instead of 8 corners + 28 FADDs.  It is 8x the node
+// grid, so it is built when it fits in the free memory minus a reserve of
+// max(4 GiB, 10% of the device) (1024^3: 137 GB of 183 GB); RAYBOS_CELL_TABLE=0
+// turns it off.  Results are bit-identical either way.
 int build_cell_table(rb_ctx* ctx, Device& dev, const rb_field_desc* desc) {
   const char* env = std::getenv("RAYBOS_CELL_TABLE");
   if (env && env[0] == '0') return RB_OK;
@@ -474,7 +484,8 @@ int build_cell_table(rb_ctx* ctx, Device& dev, const rb_field_desc* desc) {
   const size_t bytes = cells * sizeof(rbk::CellCoef);
   size_t free_b = 0, total_b = 0;
   RB_CUDA(ctx, cudaMemGetInfo(&free_b, &total_b));
-  if (bytes > free_b / 2) return RB_OK;
+  const size_t reserve = std::max<size_t>(size_t(4) << 30, total_b / 10);
+  if (bytes + reserve > free_b) return RB_OK;
   if (cudaMalloc(&dev.cells, bytes) != cudaSuccess) {
     cudaGetLastError();
     dev.cells = nullptr;
@@ -912,6 +923,15 @@ int rb_trace_rays(rb_ctx* ctx, const rb_scene* s, int with_field, int64_t n_rays
   }
   k.grid = dev.grid;
   k.cell_table = dev.cells;
+  if (k.with_field && dev.cells) {
+    // L2 prefetch on reloads pays when the cones' cells do not stay L2
+    // resident (measured: bos 256^3 +3%, 1024^3 +2.5%, tomo 256x256x128 -3%);
+    // RAYBOS_PREFETCH=0/1 overrides the size rule.
+    const char* pf = std::getenv("RAYBOS_PREFETCH");
+    k.prefetch = pf ? (pf[0] != '0') : (dev.cells_bytes > (size_t(3) << 29));
+    const double fine = std::min(k.spacing.x, std::min(k.spacing.y, k.spacing.z));
+    k.prefetch_steps = static_cast<float>(fine / k.h);
+  }
   RB_CUDA(ctx, dev.queue.ensure(sizeof(int) * 2));
   RB_CUDA(ctx, cudaMemsetAsync(dev.queue.p, 0, sizeof(int) * 2, st));
   k.err_flag = dev.queue.as<int>() + 1;

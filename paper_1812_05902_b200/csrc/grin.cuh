@@ -179,21 +179,16 @@ __device__ __forceinline__ float3 poly_eval(const CellPoly& P, float fx, float f
 #undef RB_HORNER
 }
 
-#ifndef RB_SPECULATE
-#define RB_SPECULATE 0  // measured 7% slower on tomo (duplicated Horner on reloads)
-#endif
-
+// (ax, ay, az): the ray's unperturbed advance per step in grid units; a
+// reload from the cell table also prefetches the line of the cell about one
+// cell further along the ray into L2 (KScene::prefetch), hiding the HBM
+// latency of fields larger than L2.
 template <bool kCells>
 __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, float qx, float qy,
-                                                float qz) {
+                                                float qz, float ax, float ay, float az) {
   float fx = qx - P.ox, fy = qy - P.oy, fz = qz - P.oz;
   // fast path: inside the cached cell (NaN fails and takes the full path)
   const bool stay = fminf(fminf(fx, fy), fz) >= 0.0f && fmaxf(fmaxf(fx, fy), fz) <= 1.0f;
-#if RB_SPECULATE
-  // Evaluate on the cached cell while the in-cell test resolves (it is off the
-  // critical path this way); redo only after a reload (~1 sample in 6).
-  float3 D = poly_eval(P, fx, fy, fz);
-#endif
 #if RB_UNIFORM_RELOAD
   // Warp-uniform reload: when any active lane leaves its cell, all active lanes
   // take the reload path (lanes still inside re-derive the same cell), so the
@@ -202,16 +197,17 @@ __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, 
 #else
   const bool reload = !stay;
 #endif
-#if RB_SPECULATE
   if (reload) {
     poly_load<kCells>(G, P, qx, qy, qz, fx, fy, fz);
-    D = poly_eval(P, fx, fy, fz);
+    if (kCells && G.S.prefetch) {
+      const float k = G.S.prefetch_steps;
+      const unsigned i = min(__float2uint_rz(fmaf(ax, k, qx)), G.S.g_ix);
+      const unsigned j = min(__float2uint_rz(fmaf(ay, k, qy)), G.S.g_iy);
+      const unsigned kk = min(__float2uint_rz(fmaf(az, k, qz)), G.S.g_iz);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(G.S.cell_table + (kk * G.S.c_nxny + j * G.S.c_nx + i)));
+    }
   }
-  return D;
-#else
-  if (reload) poly_load<kCells>(G, P, qx, qy, qz, fx, fy, fz);
   return poly_eval(P, fx, fy, fz);
-#endif
 }
 
 #ifndef RB_UNIFORM_RELOAD
@@ -221,7 +217,7 @@ __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, 
 #define RB_CELL_CACHE 2
 #endif
 #if RB_CELL_CACHE == 2
-#define RB_SAMPLE_D(qx, qy, qz) sample_d_poly<kCells>(G, cache, qx, qy, qz)
+#define RB_SAMPLE_D(qx, qy, qz) sample_d_poly<kCells>(G, cache, qx, qy, qz, ax, ay, az)
 #elif RB_CELL_CACHE == 1
 #define RB_SAMPLE_D(qx, qy, qz) sample_d_cached(G, cache, qx, qy, qz)
 #else

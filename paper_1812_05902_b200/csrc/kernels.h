@@ -77,6 +77,8 @@ struct KScene {
   // optional per-cell coefficient table (nullptr = derive from the nodes)
   const CellCoef* cell_table;
   unsigned c_nx, c_nxny;         // cell strides: nx - 1, (nx - 1) * (ny - 1)
+  int32_t prefetch;              // L2-prefetch the cell table one cell ahead on reloads
+  float prefetch_steps;          // RK4 steps per cell along the finest axis
   int32_t nx, ny, nz, max_steps;
   double3 origin, spacing, box_lo, box_hi;
   double h;
