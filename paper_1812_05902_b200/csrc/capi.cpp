@@ -70,6 +70,7 @@ struct Device {
   Buf f64[4];  // FP64 node copy (n, gx, gy, gz) for the validation build
   Buf qimage, dbg, dbg_n;
   Buf hit0, landed0, counters0;  // bos pair mode: the no-field leg
+  Buf hit_part, landed_part, hit_part0, landed_part0;  // split-emitter partials
 };
 
 struct NcclApi {
@@ -329,6 +330,27 @@ struct PartialOut {
   int err_flag = 0;
 };
 
+// CTAs per emitter (KScene::split).  Splitting an emitter's rays over several
+// CTAs keeps fewer distinct cones in flight, so the cells they read stay in
+// L2; each chunk costs one pilot and one tile flush.  The chunk is sized to
+// about 4e5 RK4 steps, estimating the steps per ray as the box depth along the
+// pupil axis over h (measured optimum: tomo 4-8, bos 16, 1024^3 32; bos +18%,
+// 1024^3 +4%, tomo +1% over one CTA per emitter).  No field: one CTA per
+// emitter.  RAYBOS_SPLIT overrides.
+int emitter_split(const rb_ctx* ctx, const rb_scene* s, const rbk::KScene& k) {
+  if (const char* e = std::getenv("RAYBOS_SPLIT")) return std::max(1, std::min(64, std::atoi(e)));
+  if (!k.with_field || !(k.h > 0.0)) return 1;
+  const double ext[3] = {ctx->box_hi.x - ctx->box_lo.x, ctx->box_hi.y - ctx->box_lo.y,
+                         ctx->box_hi.z - ctx->box_lo.z};
+  const double ax[3] = {s->pupil_axis.x, s->pupil_axis.y, s->pupil_axis.z};
+  const double an = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+  double depth = 0.0;
+  for (int a = 0; a < 3; ++a) depth += std::fabs(ext[a] * ax[a]) / (an > 0.0 ? an : 1.0);
+  const double steps = std::min<double>(depth / k.h, s->max_steps);
+  const double split = std::round(static_cast<double>(s->rays_per_source) * steps / 4e5);
+  return static_cast<int>(std::max(1.0, std::min(64.0, split)));
+}
+
 // One device renders the given work list into dev.image (already zeroed or
 // caller-owned when image_override != nullptr).
 // Caller-provided device buffers (rb_trace_shard's image, rb_image_from_fixed's
@@ -389,15 +411,6 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   k.err_flag = dev.queue.as<int>() + 1;
   k.grid = dev.grid;
   k.cell_table = dev.cells;
-  if (k.with_field && dev.cells) {
-    // L2 prefetch on reloads pays when the cones' cells do not stay L2
-    // resident (measured: bos 256^3 +3%, 1024^3 +2.5%, tomo 256x256x128 -3%);
-    // RAYBOS_PREFETCH=0/1 overrides the size rule.
-    const char* pf = std::getenv("RAYBOS_PREFETCH");
-    k.prefetch = pf ? (pf[0] != '0') : (dev.cells_bytes > (size_t(3) << 29));
-    const double fine = std::min(k.spacing.x, std::min(k.spacing.y, k.spacing.z));
-    k.prefetch_steps = static_cast<float>(fine / k.h);
-  }
   if (k.accumulate) {
     if (image_target) {
       k.image = image_target;
@@ -408,10 +421,28 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
     }
   }
   if (k.with_field && !dev.grid) return fail(ctx, RB_E_RUNTIME, "rb_trace: field not uploaded");
-  const int grid = std::max(1, std::min<int>(dev.sms * dev.blocks_per_sm,
-                                             std::max<int>(1, static_cast<int>(work.size()))));
+  k.split = emitter_split(ctx, s, k);
+  if (k.split > 1) {
+    const size_t units = work.size() * static_cast<size_t>(k.split);
+    RB_CUDA(ctx, dev.hit_part.ensure(sizeof(double) * 2 * units));
+    RB_CUDA(ctx, dev.landed_part.ensure(sizeof(long long) * units));
+    k.hit_part = dev.hit_part.as<double>();
+    k.landed_part = dev.landed_part.as<long long>();
+    if (k.pair) {
+      RB_CUDA(ctx, dev.hit_part0.ensure(sizeof(double) * 2 * units));
+      RB_CUDA(ctx, dev.landed_part0.ensure(sizeof(long long) * units));
+      k.hit_part0 = dev.hit_part0.as<double>();
+      k.landed_part0 = dev.landed_part0.as<long long>();
+    }
+  }
+  const int64_t units = static_cast<int64_t>(work.size()) * k.split;
+  const int grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(dev.sms * dev.blocks_per_sm, std::max<int64_t>(1, units))));
   RB_CUDA(ctx, cudaEventRecord(dev.ev0, st));
-  if (!work.empty()) RB_CUDA(ctx, rbk::launch_render(k, grid, st));
+  if (!work.empty()) {
+    RB_CUDA(ctx, rbk::launch_render(k, grid, st));
+    RB_CUDA(ctx, rbk::launch_emitter_stats(k, st));
+  }
   RB_CUDA(ctx, cudaEventRecord(dev.ev1, st));
   po.hit.assign(2 * n, 0.0);
   po.landed.assign(n, 0);
@@ -617,7 +648,9 @@ void rb_destroy(rb_ctx* ctx) {
   for (Device& d : ctx->devs) {
     free_field(d);
     for (Buf& b : d.f64) b.release();
-    for (Buf* b : {&d.qimage, &d.dbg, &d.dbg_n, &d.hit0, &d.landed0, &d.counters0}) b->release();
+    for (Buf* b : {&d.qimage, &d.dbg, &d.dbg_n, &d.hit0, &d.landed0, &d.counters0, &d.hit_part,
+                   &d.landed_part, &d.hit_part0, &d.landed_part0})
+      b->release();
     for (Buf* b : {&d.sources, &d.ids, &d.order, &d.image, &d.hit, &d.landed, &d.counters,
                    &d.queue, &d.err, &d.dimage, &d.rays_src, &d.rays_idx, &d.rays_uv,
                    &d.rays_status, &d.rays_steps})
@@ -923,15 +956,6 @@ int rb_trace_rays(rb_ctx* ctx, const rb_scene* s, int with_field, int64_t n_rays
   }
   k.grid = dev.grid;
   k.cell_table = dev.cells;
-  if (k.with_field && dev.cells) {
-    // L2 prefetch on reloads pays when the cones' cells do not stay L2
-    // resident (measured: bos 256^3 +3%, 1024^3 +2.5%, tomo 256x256x128 -3%);
-    // RAYBOS_PREFETCH=0/1 overrides the size rule.
-    const char* pf = std::getenv("RAYBOS_PREFETCH");
-    k.prefetch = pf ? (pf[0] != '0') : (dev.cells_bytes > (size_t(3) << 29));
-    const double fine = std::min(k.spacing.x, std::min(k.spacing.y, k.spacing.z));
-    k.prefetch_steps = static_cast<float>(fine / k.h);
-  }
   RB_CUDA(ctx, dev.queue.ensure(sizeof(int) * 2));
   RB_CUDA(ctx, cudaMemsetAsync(dev.queue.p, 0, sizeof(int) * 2, st));
   k.err_flag = dev.queue.as<int>() + 1;

@@ -179,13 +179,9 @@ __device__ __forceinline__ float3 poly_eval(const CellPoly& P, float fx, float f
 #undef RB_HORNER
 }
 
-// (ax, ay, az): the ray's unperturbed advance per step in grid units; a
-// reload from the cell table also prefetches the line of the cell about one
-// cell further along the ray into L2 (KScene::prefetch), hiding the HBM
-// latency of fields larger than L2.
 template <bool kCells>
 __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, float qx, float qy,
-                                                float qz, float ax, float ay, float az) {
+                                                float qz) {
   float fx = qx - P.ox, fy = qy - P.oy, fz = qz - P.oz;
   // fast path: inside the cached cell (NaN fails and takes the full path)
   const bool stay = fminf(fminf(fx, fy), fz) >= 0.0f && fmaxf(fmaxf(fx, fy), fz) <= 1.0f;
@@ -197,16 +193,7 @@ __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, 
 #else
   const bool reload = !stay;
 #endif
-  if (reload) {
-    poly_load<kCells>(G, P, qx, qy, qz, fx, fy, fz);
-    if (kCells && G.S.prefetch) {
-      const float k = G.S.prefetch_steps;
-      const unsigned i = min(__float2uint_rz(fmaf(ax, k, qx)), G.S.g_ix);
-      const unsigned j = min(__float2uint_rz(fmaf(ay, k, qy)), G.S.g_iy);
-      const unsigned kk = min(__float2uint_rz(fmaf(az, k, qz)), G.S.g_iz);
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(G.S.cell_table + (kk * G.S.c_nxny + j * G.S.c_nx + i)));
-    }
-  }
+  if (reload) poly_load<kCells>(G, P, qx, qy, qz, fx, fy, fz);
   return poly_eval(P, fx, fy, fz);
 }
 
@@ -217,7 +204,7 @@ __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, 
 #define RB_CELL_CACHE 2
 #endif
 #if RB_CELL_CACHE == 2
-#define RB_SAMPLE_D(qx, qy, qz) sample_d_poly<kCells>(G, cache, qx, qy, qz, ax, ay, az)
+#define RB_SAMPLE_D(qx, qy, qz) sample_d_poly<kCells>(G, cache, qx, qy, qz)
 #elif RB_CELL_CACHE == 1
 #define RB_SAMPLE_D(qx, qy, qz) sample_d_cached(G, cache, qx, qy, qz)
 #else

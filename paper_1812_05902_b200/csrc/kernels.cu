@@ -257,6 +257,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = S.rays;
   const int K = (S.patch_count + kWarps - 1) / kWarps;
+  const int Kc = (K + S.split - 1) / S.split;  // patch iterations per chunk
+  const int n_units = S.n_work * S.split;
   volatile double* vso = sh_so;
   volatile unsigned long long* vkey = &sh_ekey;
   volatile int* vtile = sh_tile;
@@ -264,8 +266,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
     if (tid == 0) {
       const int w = atomicAdd(S.queue, 1);
       sh_work = w;
-      if (w < S.n_work) {
-        const int src = S.order[w];
+      if (w < n_units) {
+        const int src = S.order[w / S.split];
         sh_src = src;
         const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
         sh_ekey = mix_bits(S.key_seed + sid);
@@ -285,12 +287,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
     for (int j = 0; j < 7; ++j) sh_cnt0[j][tid] = 0u;
     sh_steps[tid] = 0ull;
     __syncthreads();
-    if (sh_work >= S.n_work) break;
+    if (sh_work >= n_units) break;
+    const int kb = (sh_work % S.split) * Kc, ke = min(K, kb + Kc);
 
     // One loop, one trace_ray call site: iteration 0 is the pilot, after which
     // the CTA places the tile.  __syncwarp() reconverges the lanes after every
     // ray so a warp never splits into groups running different rays' RK4 loops.
-    for (int k = 0; k < K; ++k) {
+    for (int k = kb; k < ke; ++k) {
       int i = -1;
       const int slot = k * kWarps + warp;
       if (slot < S.patch_count) {
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
           r = trace_ray<kCells>(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid]);
         }
       }
-      if (k == 0 && S.accumulate) {  // block-uniform branch
+      if (k == kb && S.accumulate) {  // block-uniform branch
         if (r.status == 0) {  // spot_pixel_window of the pilot, clipped to the frame
           const double cc = r.u / S.pitch + 0.5 * S.W;
           const double rc = 0.5 * S.H - r.v / S.pitch;
@@ -418,9 +421,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
         for (int j = 0; j < 7; ++j) l[j] += sh_l[j][k];
       }
       const int src = sh_src;
-      S.hit_sum[2 * src] = a;
-      S.hit_sum[2 * src + 1] = b;
-      S.landed[src] = (long long)l[0];
+      double* hs = S.split > 1 ? S.hit_part + 2 * (size_t)sh_work : S.hit_sum + 2 * src;
+      hs[0] = a;
+      hs[1] = b;
+      *(S.split > 1 ? S.landed_part + sh_work : S.landed + src) = (long long)l[0];
 #pragma unroll
       for (int j = 1; j < 7; ++j)
         if (l[j]) atomicAdd(&S.counters[j - 1], l[j]);
@@ -433,15 +437,47 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
 #pragma unroll
           for (int j = 0; j < 7; ++j) m[j] += sh_l0[j][k];
         }
-        S.hit_sum0[2 * src] = a0;
-        S.hit_sum0[2 * src + 1] = b0;
-        S.landed0[src] = (long long)m[0];
+        double* hs0 = S.split > 1 ? S.hit_part0 + 2 * (size_t)sh_work : S.hit_sum0 + 2 * src;
+        hs0[0] = a0;
+        hs0[1] = b0;
+        *(S.split > 1 ? S.landed_part0 + sh_work : S.landed0 + src) = (long long)m[0];
 #pragma unroll
         for (int j = 1; j < 6; ++j)
           if (m[j]) atomicAdd(&S.counters0[j - 1], m[j]);
       }
     }
     __syncthreads();
+  }
+}
+
+// Split emitters: DotHitStats = the chunk partials summed in chunk order.
+__global__ void emitter_stats_kernel(const __grid_constant__ KScene S) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < S.n_work; e += gridDim.x * blockDim.x) {
+    const int src = S.order[e];
+    double a = 0.0, b = 0.0;
+    long long l = 0;
+    for (int c = 0; c < S.split; ++c) {
+      const size_t w = (size_t)e * S.split + c;
+      a += S.hit_part[2 * w];
+      b += S.hit_part[2 * w + 1];
+      l += S.landed_part[w];
+    }
+    S.hit_sum[2 * src] = a;
+    S.hit_sum[2 * src + 1] = b;
+    S.landed[src] = l;
+    if (S.pair) {
+      double a0 = 0.0, b0 = 0.0;
+      long long l0 = 0;
+      for (int c = 0; c < S.split; ++c) {
+        const size_t w = (size_t)e * S.split + c;
+        a0 += S.hit_part0[2 * w];
+        b0 += S.hit_part0[2 * w + 1];
+        l0 += S.landed_part0[w];
+      }
+      S.hit_sum0[2 * src] = a0;
+      S.hit_sum0[2 * src + 1] = b0;
+      S.landed0[src] = l0;
+    }
   }
 }
 
@@ -582,6 +618,12 @@ cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream) {
     else
       render_emitters<false, false><<<grid, kBlock, render_smem(), stream>>>(s);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_emitter_stats(const KScene& s, cudaStream_t stream) {
+  if (s.split <= 1 || s.n_work <= 0) return cudaSuccess;
+  emitter_stats_kernel<<<(s.n_work + 255) / 256, 256, 0, stream>>>(s);
   return cudaGetLastError();
 }
 

@@ -77,8 +77,6 @@ struct KScene {
   // optional per-cell coefficient table (nullptr = derive from the nodes)
   const CellCoef* cell_table;
   unsigned c_nx, c_nxny;         // cell strides: nx - 1, (nx - 1) * (ny - 1)
-  int32_t prefetch;              // L2-prefetch the cell table one cell ahead on reloads
-  float prefetch_steps;          // RK4 steps per cell along the finest axis
   int32_t nx, ny, nz, max_steps;
   double3 origin, spacing, box_lo, box_hi;
   double h;
@@ -114,6 +112,15 @@ struct KScene {
   double* hit_sum0;
   long long* landed0;
   unsigned long long* counters0;
+  // emitter split: `split` CTAs share one emitter's rays (fewer distinct cones
+  // in flight -> a smaller L2 working set); each writes its DotHitStats partial
+  // to part[work * split + chunk] and emitter_stats_kernel sums them in chunk
+  // order (deterministic).  split == 1 writes hit_sum / landed directly.
+  int32_t split, pad_split;
+  double* hit_part;                 // 2 * n_work * split (and *_part0 in pair mode)
+  long long* landed_part;
+  double* hit_part0;
+  long long* landed_part0;
 };
 
 // FP64 GriddedField nodes for the validation build (kernels_fp64.cu).
@@ -135,6 +142,7 @@ cudaError_t launch_quantize(const double* image, int64_t n, double gain, int bit
 cudaError_t launch_build_fp64(const float* rho, int nx, int ny, int nz, double k, double3 spacing,
                               double* n, double* gx, double* gy, double* gz, cudaStream_t stream);
 cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream);
+cudaError_t launch_emitter_stats(const KScene& s, cudaStream_t stream);
 int render_occupancy(int* blocks_per_sm);
 cudaError_t launch_trace_rays(const KScene& s, int64_t n, const int64_t* src, const int32_t* ray,
                               double* uv, int32_t* status, int32_t* steps, cudaStream_t stream);
