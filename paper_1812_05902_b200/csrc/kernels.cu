@@ -42,14 +42,16 @@ __device__ __forceinline__ bool emit_ray(const KScene& S, uint64_t ekey, double3
 }
 
 // Stages 2-4 of process_source (engine.cpp:112-137) for an emitted ray.
-template <bool kCells>
+// kField: 0 = the scene has no medium (no GRIN code at all), 1 = field read
+// from the float4 nodes, 2 = from the per-cell coefficient table.
+template <int kField>
 __device__ __forceinline__ RayResult finish_ray(const KScene& S, double3 o, double3 d, bool field,
                                                 double* scratch) {
   RayResult r;
   r.steps = 0;
   r.u = r.v = 0.0;
-  if (field) {
-    const int st = grin_trace<kCells>(S, o, d, r.steps, scratch);
+  if (kField != 0 && field) {
+    const int st = grin_trace<kField == 2>(S, o, d, r.steps, scratch);
     if (st == kLost || st == kInvalid) {
       r.status = 1;  // RB_RAY_LOST
       return r;
@@ -69,7 +71,7 @@ __device__ __forceinline__ RayResult finish_ray(const KScene& S, double3 o, doub
 }
 
 // process_source's per-ray body, engine.cpp:112-137.
-template <bool kCells>
+template <int kField>
 __device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, double3 src, int i,
                                                double* scratch) {
   double3 d;
@@ -80,7 +82,7 @@ __device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, d
     r.status = 1;
     return r;
   }
-  return finish_ray<kCells>(S, src, d, S.with_field, scratch);
+  return finish_ray<kField>(S, src, d, S.with_field, scratch);
 }
 
 // Tile-or-global fixed-point add of one pixel contribution.
@@ -116,6 +118,19 @@ __device__ __forceinline__ uint32_t dround(float x, float u) {
   return RB_DITHER ? __float2uint_rd(x + u) : __float2uint_rn(x);
 }
 
+// Shared-memory add without a return value (RED) — adding 0 is harmless, so
+// callers need no per-pixel branch.
+__device__ __forceinline__ void red_shared(uint32_t addr, uint32_t f) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(f) : "memory");
+}
+
+template <int W>
+__device__ __forceinline__ void red_row(uint32_t trow, const float (&wu)[kMaxSpot], float row_w,
+                                        float u) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) red_shared(trow + 4 * k, dround(wu[k] * row_w, u));
+}
+
 // accumulate_spot (sensor.cpp:57-122): separable erf-difference Gaussian,
 // normalized over the full window, in-frame pixels only.
 __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uint32_t* tile, int tc0,
@@ -143,6 +158,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
     float e = eu0;
 #pragma unroll
     for (int k = 0; k < kMaxSpot; ++k) {
+      wu[k] = 0.0f;  // columns past the window deposit nothing (f = floor(u) = 0)
       if (k < ncol) {
         const float en = erff(erf_arg(S, c0 + k + 1, cc));
         wu[k] = 0.5f * (en - e);
@@ -152,6 +168,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
     const float mass_u = 0.5f * (e - eu0);
     const float scale = energy_fx / (mass_u * mass_v);
     const bool cols_in_tile = c0 >= tc0 && c1 < tc0 + tw;
+    const int width = __reduce_max_sync(__activemask(), ncol);  // warp-uniform row width
     // Rows are visited starting at a lane-dependent row (wrapping once), so the
     // lanes of a coherent warp, whose spots coincide, add to different rows at
     // the same time instead of serialising on the same shared-memory words.
@@ -171,13 +188,20 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
       // (which lies in the frame): no per-pixel bounds checks.  The choice is
       // warp-uniform, so the warp never executes both loops for one row.
       if (__all_sync(__activemask(), cols_in_tile && (unsigned)(r - tr0) < (unsigned)th)) {
-        uint32_t* trow = tile + (r - tr0) * tw + (c0 - tc0);
+        // The row is `width` unconditional REDs, no branch per pixel: columns
+        // past the window have wu = 0, so they add floor(0 + u) = 0 to a word
+        // further along the tile (the allocation has kMaxSpot words of slack).
+        const uint32_t trow = (uint32_t)__cvta_generic_to_shared(tile + (r - tr0) * tw + (c0 - tc0));
+        if (width <= 4) {
 #pragma unroll
-        for (int k = 0; k < kMaxSpot; ++k) {
-          if (k < ncol) {
+          for (int k = 0; k < 4; ++k) {
             const uint32_t f = dround(wu[k] * row_w, w);
-            if (f) atomicAdd(trow + k, f);
+            if (f) red_shared(trow + 4 * k, f);
           }
+        } else if (width <= 8) {
+          red_row<8>(trow, wu, row_w, w);
+        } else {
+          red_row<kMaxSpot>(trow, wu, row_w, w);
         }
       } else {
 #pragma unroll
@@ -230,9 +254,11 @@ __device__ __forceinline__ T warp_sum(T v) {
 // whole pupil lattice).  Deposits outside the tile go straight to global.
 // kPair: bos_run pair mode (rb_trace_bos_pair), a separate instantiation so the
 // default kernel carries none of its code or registers.
-// kCells: the field is read through the per-cell coefficient table.
-template <bool kPair, bool kCells>
-__global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __grid_constant__ KScene S) {
+// kField: see finish_ray (a scene without a medium gets a kernel without the
+// GRIN loop, which keeps its instruction footprint small).
+template <bool kPair, int kField>
+__global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField : kMinBlocks)
+    render_emitters(const __grid_constant__ KScene S) {
   extern __shared__ uint32_t tile[];
   constexpr int kWarps = kBlock / 32;
   __shared__ int sh_work, sh_src;
@@ -310,19 +336,19 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) render_emitters(const __gr
           const double3 so = make_double3(vso[0], vso[1], vso[2]);
           double3 d;
           if (emit_ray(S, ekey, so, i, d)) {
-            const RayResult r0 = finish_ray<kCells>(S, so, d, false, sh_rt[tid]);
+            const RayResult r0 = finish_ray<kField>(S, so, d, false, sh_rt[tid]);
             sh_cnt0[r0.status][tid] += 1u;
             if (r0.status == 0) {
               sh_uv0[0][tid] += r0.u;
               sh_uv0[1][tid] += r0.v;
             }
-            r = finish_ray<kCells>(S, so, d, true, sh_rt[tid]);
+            r = finish_ray<kField>(S, so, d, true, sh_rt[tid]);
           } else {
             r.status = 1;
             r.steps = 0;
           }
         } else {
-          r = trace_ray<kCells>(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid]);
+          r = trace_ray<kField>(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid]);
         }
       }
       if (k == kb && S.accumulate) {  // block-uniform branch
@@ -482,7 +508,7 @@ __global__ void emitter_stats_kernel(const __grid_constant__ KScene S) {
 }
 
 // Per-ray replay (rb_trace_rays).
-template <bool kCells>
+template <int kField>
 __global__ void trace_rays_kernel(const __grid_constant__ KScene S, int64_t n,
                                   const int64_t* __restrict__ srcs, const int32_t* __restrict__ rays,
                                   double* uv, int32_t* status, int32_t* steps) {
@@ -492,7 +518,7 @@ __global__ void trace_rays_kernel(const __grid_constant__ KScene S, int64_t n,
   const int64_t src = srcs[q];
   const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
   const double3 so = make_double3(S.sources[3 * src], S.sources[3 * src + 1], S.sources[3 * src + 2]);
-  const RayResult r = trace_ray<kCells>(S, mix_bits(S.key_seed + sid), so, rays[q], sh_rt[threadIdx.x]);
+  const RayResult r = trace_ray<kField>(S, mix_bits(S.key_seed + sid), so, rays[q], sh_rt[threadIdx.x]);
   uv[2 * q] = r.status == 0 ? r.u : nan("");
   uv[2 * q + 1] = r.status == 0 ? r.v : nan("");
   status[q] = r.status;
@@ -593,30 +619,39 @@ __global__ void quantize_kernel(const double* __restrict__ img, int64_t n, doubl
 }
 
 // ------------------------------------------------ launch wrappers
-static size_t render_smem() { return (size_t)kTileCap * sizeof(uint32_t); }
+static size_t render_smem() { return (size_t)(kTileCap + kMaxSpot) * sizeof(uint32_t); }
 
-int render_occupancy(int* blocks_per_sm) {
-  const int smem = (int)render_smem();
-  cudaFuncSetAttribute(render_emitters<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(render_emitters<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(render_emitters<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(render_emitters<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      blocks_per_sm, render_emitters<false, false>, kBlock, render_smem());
+template <bool kPair, int kField>
+static void set_smem() {
+  cudaFuncSetAttribute(render_emitters<kPair, kField>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)render_smem());
 }
 
+int render_occupancy(int* blocks_per_sm, int* blocks_per_sm_no_field) {
+  set_smem<false, 0>();
+  set_smem<false, 1>();
+  set_smem<false, 2>();
+  set_smem<true, 0>();
+  set_smem<true, 1>();
+  set_smem<true, 2>();
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      blocks_per_sm, render_emitters<false, 1>, kBlock, render_smem());
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      blocks_per_sm_no_field, render_emitters<false, 0>, kBlock, render_smem());
+}
+
+static int field_mode(const KScene& s) { return !s.with_field ? 0 : (s.cell_table ? 2 : 1); }
+
 cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream) {
-  const bool cells = s.with_field && s.cell_table;
-  if (s.pair) {
-    if (cells)
-      render_emitters<true, true><<<grid, kBlock, render_smem(), stream>>>(s);
-    else
-      render_emitters<true, false><<<grid, kBlock, render_smem(), stream>>>(s);
-  } else {
-    if (cells)
-      render_emitters<false, true><<<grid, kBlock, render_smem(), stream>>>(s);
-    else
-      render_emitters<false, false><<<grid, kBlock, render_smem(), stream>>>(s);
+  const size_t sm = render_smem();
+  switch (field_mode(s) + (s.pair ? 3 : 0)) {
+    case 0: render_emitters<false, 0><<<grid, kBlock, sm, stream>>>(s); break;
+    case 1: render_emitters<false, 1><<<grid, kBlock, sm, stream>>>(s); break;
+    case 2: render_emitters<false, 2><<<grid, kBlock, sm, stream>>>(s); break;
+    case 3: render_emitters<true, 0><<<grid, kBlock, sm, stream>>>(s); break;
+    case 4: render_emitters<true, 1><<<grid, kBlock, sm, stream>>>(s); break;
+    default: render_emitters<true, 2><<<grid, kBlock, sm, stream>>>(s); break;
   }
   return cudaGetLastError();
 }
@@ -632,10 +667,11 @@ cudaError_t launch_trace_rays(const KScene& s, int64_t n, const int64_t* src, co
   if (n <= 0) return cudaSuccess;
   const int bs = 128;
   const unsigned blocks = (unsigned)((n + bs - 1) / bs);
-  if (s.with_field && s.cell_table)
-    trace_rays_kernel<true><<<blocks, bs, 0, stream>>>(s, n, src, ray, uv, status, steps);
-  else
-    trace_rays_kernel<false><<<blocks, bs, 0, stream>>>(s, n, src, ray, uv, status, steps);
+  switch (field_mode(s)) {
+    case 0: trace_rays_kernel<0><<<blocks, bs, 0, stream>>>(s, n, src, ray, uv, status, steps); break;
+    case 1: trace_rays_kernel<1><<<blocks, bs, 0, stream>>>(s, n, src, ray, uv, status, steps); break;
+    default: trace_rays_kernel<2><<<blocks, bs, 0, stream>>>(s, n, src, ray, uv, status, steps); break;
+  }
   return cudaGetLastError();
 }
 
