@@ -59,6 +59,7 @@ struct Device {
   int sms = 148;
   int blocks_per_sm = 1;
   int blocks_per_sm_nf = 1;  // render kernel of scenes without a medium
+  int blocks_per_sm_cells = 1;  // ... of fields read from the cell table
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t ev_join = nullptr;  // orders our stream after the legacy default stream
@@ -438,7 +439,8 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   }
   const int64_t units = static_cast<int64_t>(work.size()) * k.split;
   const int grid = static_cast<int>(std::max<int64_t>(
-      1, std::min<int64_t>(dev.sms * (k.with_field ? dev.blocks_per_sm : dev.blocks_per_sm_nf),
+      1, std::min<int64_t>(dev.sms * (!k.with_field ? dev.blocks_per_sm_nf
+                                      : (k.cell_table ? dev.blocks_per_sm_cells : dev.blocks_per_sm)),
                            std::max<int64_t>(1, units))));
   RB_CUDA(ctx, cudaEventRecord(dev.ev0, st));
   if (!work.empty()) {
@@ -621,9 +623,10 @@ int rb_create(int n_devices, int first_device, rb_ctx** out, char* err, size_t e
       delete ctx;
       return fail(nullptr, RB_E_CUDA, "rb_create: stream/event creation failed", err, errlen);
     }
-    if (rbk::render_occupancy(&dev.blocks_per_sm, &dev.blocks_per_sm_nf) != 0 ||
-        dev.blocks_per_sm < 1 || dev.blocks_per_sm_nf < 1)
-      dev.blocks_per_sm = dev.blocks_per_sm_nf = 1;
+    if (rbk::render_occupancy(&dev.blocks_per_sm, &dev.blocks_per_sm_nf,
+                              &dev.blocks_per_sm_cells) != 0 ||
+        dev.blocks_per_sm < 1 || dev.blocks_per_sm_nf < 1 || dev.blocks_per_sm_cells < 1)
+      dev.blocks_per_sm = dev.blocks_per_sm_nf = dev.blocks_per_sm_cells = 1;
     ctx->devs.push_back(dev);
   }
   if (n > 1) {

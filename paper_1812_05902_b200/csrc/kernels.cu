@@ -257,7 +257,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 // kField: see finish_ray (a scene without a medium gets a kernel without the
 // GRIN loop, which keeps its instruction footprint small).
 template <bool kPair, int kField>
-__global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField : kMinBlocks)
+__global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
+                                                     : (kField == 2 ? kMinBlocksCells : kMinBlocks))
     render_emitters(const __grid_constant__ KScene S) {
   extern __shared__ uint32_t tile[];
   constexpr int kWarps = kBlock / 32;
@@ -627,7 +628,7 @@ static void set_smem() {
                        (int)render_smem());
 }
 
-int render_occupancy(int* blocks_per_sm, int* blocks_per_sm_no_field) {
+int render_occupancy(int* blocks_per_sm, int* blocks_per_sm_no_field, int* blocks_per_sm_cells) {
   set_smem<false, 0>();
   set_smem<false, 1>();
   set_smem<false, 2>();
@@ -636,6 +637,9 @@ int render_occupancy(int* blocks_per_sm, int* blocks_per_sm_no_field) {
   set_smem<true, 2>();
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       blocks_per_sm, render_emitters<false, 1>, kBlock, render_smem());
+  if (e != cudaSuccess) return (int)e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm_cells, render_emitters<false, 2>,
+                                                    kBlock, render_smem());
   if (e != cudaSuccess) return (int)e;
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       blocks_per_sm_no_field, render_emitters<false, 0>, kBlock, render_smem());
