@@ -1,0 +1,83 @@
+"""Parity on the bench scenes themselves (SURVEY §8(c) at bench resolution).
+
+The golden fixtures are small; here the headline Tomo-PIV scene (256x256x128
+normal shock, thick singlet, 2048^2, ~160 RK4 steps/ray), the BOS scene (256^3
+BDT-like field, ~500 steps/ray) and the two no-medium scenes are built at their
+full grid / optics / sensor resolution with a subset of emitters and checked
+against the C oracle (bit-exact restatement of the reference, oracle/):
+  * per-ray sensor hits within 1e-3 px and identical outcomes on a ray sample
+  * the image of a few full emitters (1e3-1e4 rays each) within 1e-4 rel L2
+  * DotHitStats: identical landed counts, mean hit within 1e-3 px
+Emitters are taken evenly over the scene's list (edge and centre cones) plus the
+ones nearest x = 0, whose cones cross the Tomo shock layer."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PX_TOL = 1e-3
+IMG_RTOL = 1e-4
+
+# scene -> (build scale, emitters imaged, rays sampled per emitter)
+CASES = {"tomo": (0.01, 6, 64), "bos": (0.05, 4, 64), "optics": (0.01, 8, 64), "piv": (1.0, 24, 64)}
+
+
+def pick_emitters(scene, k):
+    """k emitters: half evenly over the list, half nearest the plane x = 0 (the
+    Tomo shock sits there, so those cones cross the gradient layer)."""
+    even = np.linspace(0, scene.n_sources - 1, k - k // 2).round().astype(int)
+    near = [i for i in np.argsort(np.abs(scene.sources[:, 0])) if i not in set(even)][: k // 2]
+    return np.concatenate([even, np.asarray(near, dtype=int)])
+
+
+def rel_l2(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / nb if nb > 0 else np.linalg.norm(a)
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def bench_scene(request, oracle):
+    from paper_1812_05902_b200 import scenes
+    name = request.param
+    scale, n_img, n_ray = CASES[name]
+    scene, grid, info, desc = scenes.build(name, scale=scale)
+    pick = pick_emitters(scene, n_img)
+    if scene.source_ids is None:
+        scene.source_ids = np.arange(scene.n_sources, dtype=np.int64)
+    scene.sources = scene.sources[pick].copy()
+    scene.source_ids = scene.source_ids[pick].copy()  # keep each emitter's RNG stream
+    field = oracle.field_from_density(grid) if grid is not None else None
+    return name, scene, grid, field, n_ray
+
+
+def test_bench_scene_rays_match_oracle(tracer, oracle, bench_scene):
+    name, scene, grid, field, n_ray = bench_scene
+    tracer.set_field(grid)
+    rng = np.random.default_rng(11)
+    src = np.repeat(np.arange(scene.n_sources), n_ray)
+    ray = rng.integers(0, scene.rays_per_source, src.size).astype(np.int32)
+    uv, status, steps = tracer.trace_rays(scene, src, ray, grid is not None)
+    ruv, rstatus, rsteps, _ = oracle.trace_rays(scene, field, src, ray, grid is not None)
+    assert np.array_equal(status, rstatus)
+    ok = status == 0
+    assert ok.mean() > 0.5, f"{name}: too few rays land for a meaningful check"
+    err = np.abs(uv[ok] - ruv[ok]).max() / scene.sensor.pitch
+    assert err < PX_TOL, (name, err)
+    if grid is not None:
+        assert np.abs(steps - rsteps).max() <= 1
+        assert steps[ok].mean() > 50  # the rays really cross the medium
+
+
+def test_bench_scene_image_matches_oracle(tracer, oracle, bench_scene):
+    name, scene, grid, field, _ = bench_scene
+    tracer.set_field(grid)
+    a = tracer.run_trace(scene, grid is not None, True)
+    b = oracle.trace(scene, field, grid is not None, True)
+    assert a.report["emitted"] == b.report["emitted"]
+    assert np.array_equal(a.landed, b.landed)
+    for k in ("lost", "blocked_aperture", "blocked_miss", "blocked_tir", "blocked_sensor_miss"):
+        assert a.report[k] == b.report[k], k
+    m = a.landed > 0
+    d = np.abs(a.hit_sum[m] / a.landed[m, None] - b.hit_sum[m] / b.landed[m, None]).max()
+    assert d / scene.sensor.pitch < PX_TOL, (name, d)
+    assert rel_l2(a.image, b.image) < IMG_RTOL, (name, rel_l2(a.image, b.image))
