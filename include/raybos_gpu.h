@@ -193,6 +193,16 @@ int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, 
  * the central / one-sided differences in FP64 — and packs the same float4 grid. */
 int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rho,
                          double gladstone_dale_k);
+/* A GVOL file (load_density_volume, scene.cpp:212-240: "GVOL1 nx ny nz dx dy dz
+ * ox oy oz\n" + little-endian float32, x fastest) streamed to the devices in
+ * z-slabs of at most `slab_bytes` (<= 0: 64 MiB) through two pinned buffers, so
+ * host memory stays at two slabs for any volume size; the GriddedField ctor then
+ * runs on device as in rb_set_field_density.  `z_center` non-NULL recentres the
+ * volume on (0, 0, *z_center) like build_medium_volume (engine.cpp:27-37).  The
+ * resolved grid geometry is written to `desc_out` (may be NULL).  Error messages
+ * and their order are the reference's. */
+int rb_set_field_gvol(rb_ctx* ctx, const char* path, const double* z_center,
+                      double gladstone_dale_k, int64_t slab_bytes, rb_field_desc* desc_out);
 int rb_clear_field(rb_ctx* ctx);
 /* Bytes of device memory held by the packed grid (and its per-cell coefficient
  * table, when one was built) on each device. */

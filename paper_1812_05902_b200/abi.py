@@ -107,6 +107,7 @@ EXPORTED_SYMBOLS = (
     "rb_set_field_nodes", "rb_set_field_density", "rb_clear_field", "rb_field_bytes",
     "rb_trace", "rb_plan_shards", "rb_trace_shard", "rb_image_from_fixed", "rb_trace_rays",
     "rb_trace_rays_fp64", "rb_trace_stats_fp64", "rb_trace_debug", "rb_trace_bos_pair",
+    "rb_set_field_gvol",
 )
 
 _lib = None
@@ -139,6 +140,9 @@ def load_library(path: str | None = None) -> C.CDLL:
     lib.rb_set_field_density.argtypes = [C.c_void_p, C.POINTER(FieldDesc), C.POINTER(C.c_float),
                                          C.c_double]
     lib.rb_set_field_density.restype = C.c_int
+    lib.rb_set_field_gvol.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_double), C.c_double,
+                                      C.c_int64, C.POINTER(FieldDesc)]
+    lib.rb_set_field_gvol.restype = C.c_int
     lib.rb_clear_field.argtypes = [C.c_void_p]
     lib.rb_clear_field.restype = C.c_int
     lib.rb_field_bytes.argtypes = [C.c_void_p]

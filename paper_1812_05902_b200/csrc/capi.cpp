@@ -15,10 +15,13 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <numeric>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -708,6 +711,36 @@ int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, 
   return RB_OK;
 }
 
+// GriddedField ctor (scene.cpp:53-92) on device from a device-resident density
+// volume: the float4 grid, the cell table and (small grids) the FP64 nodes.
+int build_from_device_rho(rb_ctx* ctx, Device& dev, const rb_field_desc* desc, Buf& drho,
+                          double k) {
+  const size_t count = static_cast<size_t>(desc->nx) * desc->ny * desc->nz;
+  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+  RB_CUDA(ctx, rbk::launch_build_from_density(drho.as<float>(), desc->nx, desc->ny, desc->nz, k,
+                                              d3(desc->spacing), dev.grid, 0, desc->nz,
+                                              dev.stream));
+  if (int rc = build_cell_table(ctx, dev, desc)) return rc;
+  for (Buf& b : dev.f64) b.release();
+  if (static_cast<long long>(count) <= RB_FP64_MAX_NODES) {
+    for (Buf& b : dev.f64) RB_CUDA(ctx, b.ensure(count * sizeof(double)));
+    RB_CUDA(ctx, rbk::launch_build_fp64(drho.as<float>(), desc->nx, desc->ny, desc->nz, k,
+                                        d3(desc->spacing), dev.f64[0].as<double>(),
+                                        dev.f64[1].as<double>(), dev.f64[2].as<double>(),
+                                        dev.f64[3].as<double>(), dev.stream));
+  }
+  RB_CUDA(ctx, cudaStreamSynchronize(dev.stream));
+  drho.release();
+  set_l2_window(dev);
+  return RB_OK;
+}
+
+bool valid_density(const float* rho, size_t n) {  // DensityVolume::validate, scene.cpp:30-33
+  for (size_t q = 0; q < n; ++q)
+    if (!std::isfinite(rho[q]) || rho[q] < 0.0f) return false;
+  return true;
+}
+
 int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rho,
                          double gladstone_dale_k) {
   if (!ctx) return RB_E_INVALID;
@@ -716,32 +749,120 @@ int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rh
   if (gladstone_dale_k <= 0.0)
     return fail(ctx, RB_E_INVALID, "gladstone_dale: K must be positive");  // scene.cpp:18
   const size_t count = static_cast<size_t>(desc->nx) * desc->ny * desc->nz;
-  for (size_t q = 0; q < count; ++q)  // DensityVolume::validate, scene.cpp:30-33
-    if (!std::isfinite(rho[q]) || rho[q] < 0.0f)
-      return fail(ctx, RB_E_INVALID, "DensityVolume: densities must be finite and >= 0");
+  if (!valid_density(rho, count))
+    return fail(ctx, RB_E_INVALID, "DensityVolume: densities must be finite and >= 0");
   for (Device& dev : ctx->devs) {
     if (int rc = upload_grid(ctx, dev, count)) return rc;
     Buf drho;
     RB_CUDA(ctx, drho.ensure(count * sizeof(float)));
     RB_CUDA(ctx, cudaMemcpyAsync(drho.p, rho, count * sizeof(float), cudaMemcpyHostToDevice,
                                  dev.stream));
-    RB_CUDA(ctx, rbk::launch_build_from_density(drho.as<float>(), desc->nx, desc->ny, desc->nz,
-                                                gladstone_dale_k, d3(desc->spacing), dev.grid, 0,
-                                                desc->nz, dev.stream));
-    if (int rc = build_cell_table(ctx, dev, desc)) return rc;
-    for (Buf& b : dev.f64) b.release();
-    if (static_cast<long long>(count) <= RB_FP64_MAX_NODES) {
-      for (Buf& b : dev.f64) RB_CUDA(ctx, b.ensure(count * sizeof(double)));
-      RB_CUDA(ctx, rbk::launch_build_fp64(drho.as<float>(), desc->nx, desc->ny, desc->nz,
-                                          gladstone_dale_k, d3(desc->spacing), dev.f64[0].as<double>(),
-                                          dev.f64[1].as<double>(), dev.f64[2].as<double>(),
-                                          dev.f64[3].as<double>(), dev.stream));
-    }
-    RB_CUDA(ctx, cudaStreamSynchronize(dev.stream));
-    drho.release();
-    set_l2_window(dev);
+    if (int rc = build_from_device_rho(ctx, dev, desc, drho, gladstone_dale_k)) return rc;
   }
   set_box(ctx, desc);
+  return RB_OK;
+}
+
+// load_density_volume (scene.cpp:212-240) streamed: the file is read in z-slabs
+// into two pinned buffers, each copied to every device while the next is read,
+// so host memory stays at two slabs whatever the volume size; the GriddedField
+// ctor then runs on device.  Errors and their order follow the reference
+// (open, header, dims/spacing, truncation, then DensityVolume::validate).
+int rb_set_field_gvol(rb_ctx* ctx, const char* path, const double* z_center,
+                      double gladstone_dale_k, int64_t slab_bytes, rb_field_desc* desc_out) {
+  if (!ctx) return RB_E_INVALID;
+  if (!path) return fail(ctx, RB_E_INVALID, "rb_set_field_gvol: path is NULL");
+  const std::string p(path);
+  if (gladstone_dale_k <= 0.0)
+    return fail(ctx, RB_E_INVALID, "gladstone_dale: K must be positive");
+  std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(path, "rb"), &std::fclose);
+  if (!f) return fail(ctx, RB_E_INVALID, "load_density_volume: cannot open " + p);
+  std::string header;
+  int ch;
+  while ((ch = std::fgetc(f.get())) != EOF && ch != '\n') header.push_back(static_cast<char>(ch));
+  if (header.empty() && ch == EOF)
+    return fail(ctx, RB_E_INVALID, "load_density_volume: missing header in " + p);
+  std::istringstream hs(header);
+  std::string magic;
+  rb_field_desc d{};
+  hs >> magic >> d.nx >> d.ny >> d.nz >> d.spacing.x >> d.spacing.y >> d.spacing.z >> d.origin.x >>
+      d.origin.y >> d.origin.z;
+  if (!hs || magic != "GVOL1")
+    return fail(ctx, RB_E_INVALID, "load_density_volume: malformed GVOL header in " + p);
+  if (d.nx < 2 || d.ny < 2 || d.nz < 2 || d.spacing.x <= 0 || d.spacing.y <= 0 || d.spacing.z <= 0)
+    return fail(ctx, RB_E_INVALID, "load_density_volume: invalid dims/spacing in " + p);
+  if (z_center) {  // build_medium_volume (engine.cpp:33-37): recentre on (0, 0, z_center)
+    // Aabb center of DensityVolume::bounds (scene.hpp:34-36, core.hpp:77), same op order
+    const double hi[3] = {d.origin.x + (d.nx - 1) * d.spacing.x, d.origin.y + (d.ny - 1) * d.spacing.y,
+                          d.origin.z + (d.nz - 1) * d.spacing.z};
+    const double c[3] = {(d.origin.x + hi[0]) * 0.5, (d.origin.y + hi[1]) * 0.5,
+                         (d.origin.z + hi[2]) * 0.5};
+    d.origin.x += 0.0 - c[0];
+    d.origin.y += 0.0 - c[1];
+    d.origin.z += *z_center - c[2];
+  }
+  if (int rc = check_field_desc(ctx, &d)) return rc;
+  ctx->has_field = ctx->has_field64 = false;  // the old grid goes now
+  const size_t plane = static_cast<size_t>(d.nx) * d.ny;
+  const size_t count = plane * d.nz;
+  const size_t want = slab_bytes > 0 ? static_cast<size_t>(slab_bytes) : (size_t(64) << 20);
+  const size_t planes = std::max<size_t>(1, std::min<size_t>(d.nz, want / (plane * 4)));
+  std::vector<Buf> drho(ctx->devs.size());
+  for (size_t i = 0; i < ctx->devs.size(); ++i) {
+    if (int rc = upload_grid(ctx, ctx->devs[i], count)) return rc;
+    RB_CUDA(ctx, drho[i].ensure(count * sizeof(float)));
+  }
+  float* pinned[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> done[2];
+  struct Cleanup {
+    float** p;
+    std::vector<cudaEvent_t>* e;
+    ~Cleanup() {
+      for (int b = 0; b < 2; ++b) {
+        for (cudaEvent_t x : e[b]) {
+          cudaEventSynchronize(x);
+          cudaEventDestroy(x);
+        }
+        if (p[b]) cudaFreeHost(p[b]);
+      }
+    }
+  } cleanup{pinned, done};
+  for (int b = 0; b < 2; ++b) {
+    RB_CUDA(ctx, cudaHostAlloc(reinterpret_cast<void**>(&pinned[b]), planes * plane * sizeof(float),
+                               cudaHostAllocPortable));
+    for (Device& dev : ctx->devs) {
+      RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+      cudaEvent_t e;
+      RB_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      done[b].push_back(e);
+    }
+  }
+  bool valid = true;
+  bool used[2] = {false, false};
+  int b = 0;
+  for (size_t z0 = 0; z0 < static_cast<size_t>(d.nz); z0 += planes, b ^= 1) {
+    const size_t nz = std::min(planes, static_cast<size_t>(d.nz) - z0);
+    const size_t n = nz * plane;
+    if (used[b])  // the copies out of this buffer must be done before refilling it
+      for (cudaEvent_t e : done[b]) RB_CUDA(ctx, cudaEventSynchronize(e));
+    if (std::fread(pinned[b], sizeof(float), n, f.get()) != n)
+      return fail(ctx, RB_E_INVALID, "load_density_volume: truncated data in " + p);
+    // GVOL data are little-endian float32, the host's own layout (x86-64 / aarch64)
+    valid = valid && valid_density(pinned[b], n);
+    for (size_t i = 0; i < ctx->devs.size(); ++i) {
+      Device& dev = ctx->devs[i];
+      RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+      RB_CUDA(ctx, cudaMemcpyAsync(drho[i].as<float>() + z0 * plane, pinned[b], n * sizeof(float),
+                                   cudaMemcpyHostToDevice, dev.stream));
+      RB_CUDA(ctx, cudaEventRecord(done[b][i], dev.stream));
+    }
+    used[b] = true;
+  }
+  if (!valid) return fail(ctx, RB_E_INVALID, "DensityVolume: densities must be finite and >= 0");
+  for (size_t i = 0; i < ctx->devs.size(); ++i)
+    if (int rc = build_from_device_rho(ctx, ctx->devs[i], &d, drho[i], gladstone_dale_k)) return rc;
+  set_box(ctx, &d);
+  if (desc_out) *desc_out = d;
   return RB_OK;
 }
 

@@ -8,6 +8,7 @@ never runs in Python and there is no CPU fallback (constructing a
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional, Union
 
 import numpy as np
@@ -86,6 +87,19 @@ class GpuTracer:
                                                float(field.gladstone_dale))
         if rc:
             _raise(self.lib, self.ctx, rc, "set_field")
+
+    def set_field_gvol(self, path: str, gladstone_dale: float = 2.26e-4,
+                       z_center: Optional[float] = None, slab_bytes: int = 0) -> abi.FieldDesc:
+        """rb_set_field_gvol: stream a GVOL file to the devices (host memory stays
+        at two z-slabs) and build the grid there; returns the grid geometry."""
+        d = abi.FieldDesc()
+        zc = C.c_double(z_center) if z_center is not None else None
+        rc = self.lib.rb_set_field_gvol(self.ctx, os.fsencode(path),
+                                        C.byref(zc) if zc is not None else None,
+                                        float(gladstone_dale), int(slab_bytes), C.byref(d))
+        if rc:
+            _raise(self.lib, self.ctx, rc, "set_field_gvol")
+        return d
 
     def field_bytes(self) -> int:
         return int(self.lib.rb_field_bytes(self.ctx))
