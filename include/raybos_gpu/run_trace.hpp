@@ -21,6 +21,7 @@
 #pragma once
 
 #include <cmath>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -57,6 +58,7 @@ struct Context {
   // allocated where a freed one lived).
   std::weak_ptr<const raybos::GriddedField> field;
   bool has_field = false;
+  bool external = false;  // grid streamed by load_medium_gvol, no host GriddedField
   std::mutex mu;
 
   Context() {
@@ -70,6 +72,7 @@ struct Context {
 
   void ensure_field(const std::shared_ptr<const raybos::GriddedField>& sp) {
     if (has_field && !field.expired() && field.lock() == sp) return;
+    external = false;
     if (!sp) {
       rb_clear_field(ctx);
       field.reset();
@@ -210,6 +213,7 @@ inline raybos::TraceOutputs run_trace(const raybos::SceneSetup& setup, bool with
   detail::Context& C = detail::context();
   std::lock_guard<std::mutex> lock(C.mu);
   if (with_field && setup.field) C.ensure_field(setup.field);
+  const bool field = with_field && (setup.field || C.external);
   detail::FlatScene f;
   detail::flatten(setup, f);
   raybos::TraceOutputs out;
@@ -220,10 +224,41 @@ inline raybos::TraceOutputs run_trace(const raybos::SceneSetup& setup, bool with
   o.hit_sum = hit.data();
   o.landed = landed.data();
   o.image = accumulate_image ? out.image.data.data() : nullptr;
-  const int rc = rb_trace(C.ctx, &f.s, (with_field && setup.field) ? 1 : 0, accumulate_image ? 1 : 0, &o);
+  const int rc = rb_trace(C.ctx, &f.s, field ? 1 : 0, accumulate_image ? 1 : 0, &o);
   if (rc) detail::raise(rc, rb_last_error(C.ctx));
   detail::unflatten(o, hit, landed, out);
   return out;
+}
+
+// The config's GVOL medium streamed straight to the devices (rb_set_field_gvol),
+// recentred like build_medium_volume (engine.cpp:27-37), for volumes whose host
+// GriddedField would not fit (1024^3: 34 GB).  Build `setup` with
+// build_scene_setup from a copy of the config with medium.type = "none"; this
+// then fills in what build_scene_setup derives from the volume (step size,
+// max_steps and the BOS depth, engine.cpp:237-252), and run_trace(setup, true,
+// ...) traces through the streamed grid while setup.field stays empty.
+inline void load_medium_gvol(const raybos::ExperimentConfig& cfg, raybos::SceneSetup& setup) {
+  if (cfg.medium.type != "gvol") throw std::runtime_error("raybos_gpu: medium is not gvol");
+  detail::Context& C = detail::context();
+  std::lock_guard<std::mutex> lock(C.mu);
+  C.field.reset();
+  C.has_field = false;
+  C.external = false;
+  const double zc = cfg.geometry.z_dot_to_volume;
+  rb_field_desc d{};
+  const int rc = rb_set_field_gvol(C.ctx, cfg.medium.path.c_str(), &zc, cfg.gladstone_dale, 0, &d);
+  if (rc) detail::raise(rc, rb_last_error(C.ctx));
+  C.external = true;
+  const raybos::Vec3 sp{d.spacing.x, d.spacing.y, d.spacing.z};
+  const raybos::Vec3 lo{d.origin.x, d.origin.y, d.origin.z};
+  const raybos::Vec3 hi = lo + raybos::Vec3{(d.nx - 1) * sp.x, (d.ny - 1) * sp.y, (d.nz - 1) * sp.z};
+  setup.bos_params.depth = (d.nz - 1) * sp.z;
+  setup.step.delta_xi =
+      cfg.trace.delta_xi > 0.0 ? cfg.trace.delta_xi : 0.5 * std::min({sp.x, sp.y, sp.z});
+  if (cfg.trace.max_steps > 0)
+    setup.step.max_steps = cfg.trace.max_steps;
+  else
+    setup.step.max_steps = static_cast<int>(4.0 * raybos::norm(hi - lo) / setup.step.delta_xi) + 64;
 }
 
 // bos_run's two traces (engine.cpp:539-540, write_images off) in one fused

@@ -16,6 +16,7 @@
 
 #include "raybos/bos.hpp"
 #include "raybos/engine.hpp"
+#include "raybos/scene.hpp"
 #include "raybos/sensor.hpp"
 #include "raybos/validate.hpp"
 #include "raybos_gpu/run_trace.hpp"
@@ -39,11 +40,12 @@ std::string num(const char* k, double v) {
   return b;
 }
 
-void compare_traces(const std::string& name, const SceneSetup& setup, bool with_field) {
+void compare_traces(const std::string& name, const SceneSetup& setup, bool with_field,
+                    const SceneSetup* gpu_setup = nullptr) {
   RunConfig run;
   run.threads = 0;
   const TraceOutputs ref = raybos::run_trace(setup, with_field, true, run);
-  const TraceOutputs gpu = raybos_gpu::run_trace(setup, with_field, true, run);
+  const TraceOutputs gpu = raybos_gpu::run_trace(gpu_setup ? *gpu_setup : setup, with_field, true, run);
   const RunReport& a = ref.report;
   const RunReport& b = gpu.report;
   const bool counters = a.emitted == b.emitted && a.landed == b.landed && a.lost == b.lost &&
@@ -169,6 +171,39 @@ int main() {
     compare_traces(c.name, setup, true);
     if (std::string(c.name) == "small" || std::string(c.name) == "determinism")
       compare_traces(c.name, setup, false);
+  }
+  {  // GVOL medium: the reference loads it into a host GriddedField; the drop-in
+     // streams the file to the GPU (load_medium_gvol) and never builds one
+    DensityVolume vol;
+    vol.nx = 40;
+    vol.ny = 36;
+    vol.nz = 24;
+    vol.spacing = {4e-4, 4.5e-4, 5e-4};
+    vol.origin = {0.003, -0.002, 0.1};  // recentred by build_medium_volume
+    vol.rho.resize(static_cast<size_t>(vol.nx) * vol.ny * vol.nz);
+    for (int k = 0; k < vol.nz; ++k)
+      for (int j = 0; j < vol.ny; ++j)
+        for (int i = 0; i < vol.nx; ++i) {
+          const double x = (i - 17.0) / 7.0, y = (j - 19.0) / 6.0, z = (k - 11.0) / 5.0;
+          vol.rho[vol.index(i, j, k)] = static_cast<float>(1.2 + 3.0 * std::exp(-(x * x + y * y + z * z)));
+        }
+    const std::string path = "/tmp/raybos_adapter_parity.gvol";
+    save_density_volume(vol, path);
+    ExperimentConfig cfg = make_bos_blob_config();
+    cfg.medium.type = "gvol";
+    cfg.medium.path = path;
+    const SceneSetup ref_setup = build_scene_setup(cfg);
+    ExperimentConfig none = cfg;
+    none.medium.type = "none";
+    SceneSetup gpu_setup = build_scene_setup(none);
+    raybos_gpu::load_medium_gvol(cfg, gpu_setup);
+    const bool same = gpu_setup.step.delta_xi == ref_setup.step.delta_xi &&
+                      gpu_setup.step.max_steps == ref_setup.step.max_steps &&
+                      gpu_setup.bos_params.depth == ref_setup.bos_params.depth && !gpu_setup.field;
+    check("gvol_stream/setup", same,
+          num("delta_xi", gpu_setup.step.delta_xi) + ", " + num("max_steps", gpu_setup.step.max_steps));
+    compare_traces("gvol_stream", ref_setup, true, &gpu_setup);
+    std::remove(path.c_str());
   }
   compare_bos("bos_uniform", make_bos_uniform_config());
   compare_bos("bos_blob", make_bos_blob_config());
