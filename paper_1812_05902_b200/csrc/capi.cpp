@@ -60,9 +60,7 @@ struct Buf {
 struct Device {
   int ordinal = 0;
   int sms = 148;
-  int blocks_per_sm = 1;
-  int blocks_per_sm_nf = 1;  // render kernel of scenes without a medium
-  int blocks_per_sm_cells = 1;  // ... of fields read from the cell table
+  int blocks_per_sm[2][3] = {{1, 1, 1}, {1, 1, 1}};  // render kernel, [pair][field mode]
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t ev_join = nullptr;  // orders our stream after the legacy default stream
@@ -442,8 +440,7 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   }
   const int64_t units = static_cast<int64_t>(work.size()) * k.split;
   const int grid = static_cast<int>(std::max<int64_t>(
-      1, std::min<int64_t>(dev.sms * (!k.with_field ? dev.blocks_per_sm_nf
-                                      : (k.cell_table ? dev.blocks_per_sm_cells : dev.blocks_per_sm)),
+      1, std::min<int64_t>(dev.sms * dev.blocks_per_sm[k.pair ? 1 : 0][rbk::field_mode(k)],
                            std::max<int64_t>(1, units))));
   RB_CUDA(ctx, cudaEventRecord(dev.ev0, st));
   if (!work.empty()) {
@@ -535,25 +532,34 @@ int build_cell_table(rb_ctx* ctx, Device& dev, const rb_field_desc* desc) {
   return RB_OK;
 }
 
-// Keeps the field hot in L2 with an access-policy window on the render stream.
+// Keeps the field hot in L2 with an access-policy window on the render stream
+// when it fits the persisting carve-out.  A window over a field larger than
+// that (the bench scenes' cell tables, 1-137 GB) gave no speedup (the emitter
+// split already keeps the cones' cells at 97% L2 hits) and its persisting
+// lines pushed the render kernel's spill lines out to DRAM (2.5 GB of
+// write-backs per 1e8 Tomo rays, 23 MB without it), so it is left off there.
+// RAYBOS_L2_WINDOW=0 / 1 forces it off / on.
 void set_l2_window(Device& dev) {
   cudaSetDevice(dev.ordinal);
   int max_persist = 0, max_window = 0;
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev.ordinal);
   cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev.ordinal);
-  if (max_persist <= 0 || max_window <= 0 || !dev.grid) return;
-  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(max_persist));
-  cudaStreamAttrValue attr{};
   void* base = dev.cells ? static_cast<void*>(dev.cells) : static_cast<void*>(dev.grid);
   const size_t bytes = dev.cells ? dev.cells_bytes : dev.grid_bytes;
-  const size_t win = std::min<size_t>(bytes, static_cast<size_t>(max_window));
-  attr.accessPolicyWindow.base_ptr = base;
-  attr.accessPolicyWindow.num_bytes = win;
-  attr.accessPolicyWindow.hitRatio =
-      std::min(1.0f, static_cast<float>(max_persist) / static_cast<float>(win));
-  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  cudaStreamSetAttribute(dev.stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+  const char* e = std::getenv("RAYBOS_L2_WINDOW");
+  const bool on = e ? e[0] != '0' : bytes <= static_cast<size_t>(std::max(max_persist, 0));
+  cudaStreamAttrValue attr{};
+  if (on && max_persist > 0 && max_window > 0 && base) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(max_persist));
+    const size_t win = std::min<size_t>(bytes, static_cast<size_t>(max_window));
+    attr.accessPolicyWindow.base_ptr = base;
+    attr.accessPolicyWindow.num_bytes = win;
+    attr.accessPolicyWindow.hitRatio =
+        std::min(1.0f, static_cast<float>(max_persist) / static_cast<float>(win));
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  }
+  cudaStreamSetAttribute(dev.stream, cudaStreamAttributeAccessPolicyWindow, &attr);  // or clear it
   cudaGetLastError();  // the window is a hint; never fail on it
 }
 
@@ -626,10 +632,9 @@ int rb_create(int n_devices, int first_device, rb_ctx** out, char* err, size_t e
       delete ctx;
       return fail(nullptr, RB_E_CUDA, "rb_create: stream/event creation failed", err, errlen);
     }
-    if (rbk::render_occupancy(&dev.blocks_per_sm, &dev.blocks_per_sm_nf,
-                              &dev.blocks_per_sm_cells) != 0 ||
-        dev.blocks_per_sm < 1 || dev.blocks_per_sm_nf < 1 || dev.blocks_per_sm_cells < 1)
-      dev.blocks_per_sm = dev.blocks_per_sm_nf = dev.blocks_per_sm_cells = 1;
+    rbk::render_occupancy(dev.blocks_per_sm);
+    for (auto& row : dev.blocks_per_sm)
+      for (int& b : row) b = std::max(b, 1);
     ctx->devs.push_back(dev);
   }
   if (n > 1) {

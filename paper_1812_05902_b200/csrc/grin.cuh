@@ -262,9 +262,9 @@ __device__ __forceinline__ bool aabb_intersect(const KScene& S, double3 o, doubl
 // scratch: 7 doubles of shared memory for this thread; R0 and T0 are parked
 // there during the RK4 loop (they are only needed again at the exit).
 template <bool kCells>
-__device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& d, int& steps,
+__device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& d,
+                                          unsigned long long* steps_acc,
                                           double* scratch) {
-  steps = 0;
   double tn;
   if (!aabb_intersect(S, o, d, tn)) return kMissed;
   if (!(S.h > 0.0)) return kInvalid;
@@ -304,8 +304,13 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
 #define RB_STEP_UNROLL 1
 #endif
   constexpr int kStepUnroll = RB_STEP_UNROLL;
+  // The step count goes straight into the caller's (shared-memory) counter
+  // after the loop: returned as a value it was spilled, and the compiler sank
+  // the spill store into the loop (two local stores per RK4 step).
+  int status = kLost;
+  int step = 0;
 #pragma unroll kStepUnroll
-  for (int step = 0; step < max_steps; ++step) {
+  for (; step < max_steps; ++step) {
     const float fs = (float)step;
     const float pbx = fmaf(ax, fs + 0.5f, q0x), pby = fmaf(ay, fs + 0.5f, q0y),
                 pbz = fmaf(az, fs + 0.5f, q0z);
@@ -341,8 +346,8 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
     }
     if (!(isfinite(ndrx) && isfinite(ndry) && isfinite(ndrz) && isfinite(ndtx) &&
           isfinite(ndty) && isfinite(ndtz))) {
-      steps = step;
-      return kInvalid;  // grin.cpp:99
+      status = kInvalid;  // grin.cpp:99
+      break;
     }
     // Crossed the boundary: cut back to the first face crossing (grin.cpp:110-130),
     // evaluated on the FP64 reconstruction of both states.
@@ -372,10 +377,10 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
     s = fmin(fmax(s, 0.0), 1.0);
     o = r0 + (r1 - r0) * s;
     d = normalized(t0 + (t1 - t0) * s);
-    steps = step + 1;
-    return kTraced;
+    status = kTraced;
+    break;
   }
-  steps = max_steps;
-  return kLost;
+  *steps_acc += (unsigned long long)(step + (status == kTraced ? 1 : 0));  // kLost: step == max_steps
+  return status;
 }
 

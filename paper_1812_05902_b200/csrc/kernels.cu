@@ -22,7 +22,7 @@ namespace {
 
 struct RayResult {
   double u, v;
-  int status, steps;
+  int status;
 };
 
 // process_source's per-ray body, engine.cpp:112-137.
@@ -44,14 +44,14 @@ __device__ __forceinline__ bool emit_ray(const KScene& S, uint64_t ekey, double3
 // Stages 2-4 of process_source (engine.cpp:112-137) for an emitted ray.
 // kField: 0 = the scene has no medium (no GRIN code at all), 1 = field read
 // from the float4 nodes, 2 = from the per-cell coefficient table.
+// The ray's RK4 steps are added to *steps_acc.
 template <int kField>
 __device__ __forceinline__ RayResult finish_ray(const KScene& S, double3 o, double3 d, bool field,
-                                                double* scratch) {
+                                                double* scratch, unsigned long long* steps_acc) {
   RayResult r;
-  r.steps = 0;
   r.u = r.v = 0.0;
   if (kField != 0 && field) {
-    const int st = grin_trace<kField == 2>(S, o, d, r.steps, scratch);
+    const int st = grin_trace<kField == 2>(S, o, d, steps_acc, scratch);
     if (st == kLost || st == kInvalid) {
       r.status = 1;  // RB_RAY_LOST
       return r;
@@ -73,16 +73,15 @@ __device__ __forceinline__ RayResult finish_ray(const KScene& S, double3 o, doub
 // process_source's per-ray body, engine.cpp:112-137.
 template <int kField>
 __device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, double3 src, int i,
-                                               double* scratch) {
+                                               double* scratch, unsigned long long* steps_acc) {
   double3 d;
   if (!emit_ray(S, ekey, src, i, d)) {
     RayResult r;
     r.u = r.v = 0.0;
-    r.steps = 0;
     r.status = 1;
     return r;
   }
-  return finish_ray<kField>(S, src, d, S.with_field, scratch);
+  return finish_ray<kField>(S, src, d, S.with_field, scratch, steps_acc);
 }
 
 // Tile-or-global fixed-point add of one pixel contribution.
@@ -124,6 +123,23 @@ __device__ __forceinline__ void red_shared(uint32_t addr, uint32_t f) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(f) : "memory");
 }
 
+// Reloads chunks [0, n) of the column weights (volatile: must not be hoisted
+// out of the row loop, or they would stay in registers again).
+__device__ __forceinline__ void lds_weights(const float4* wsh, float (&wr)[kMaxSpot], int n) {
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < n)
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w)
+                   : "r"((uint32_t)__cvta_generic_to_shared(wsh + j * kBlock)));
+    wr[4 * j] = q.x;
+    wr[4 * j + 1] = q.y;
+    wr[4 * j + 2] = q.z;
+    wr[4 * j + 3] = q.w;
+  }
+}
+
 template <int W>
 __device__ __forceinline__ void red_row(uint32_t trow, const float (&wu)[kMaxSpot], float row_w,
                                         float u) {
@@ -133,8 +149,11 @@ __device__ __forceinline__ void red_row(uint32_t trow, const float (&wu)[kMaxSpo
 
 // accumulate_spot (sensor.cpp:57-122): separable erf-difference Gaussian,
 // normalized over the full window, in-frame pixels only.
+// wsh: this thread's 3 float4 slots (stride kBlock) of shared memory for the
+// column weights; the row loop re-reads them (3 LDS.128 per row) instead of
+// holding 12 registers across it, which at 80 registers spilled them.
 __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uint32_t* tile, int tc0,
-                                     int tr0, int tw, int th, uint32_t seed) {
+                                     int tr0, int tw, int th, uint32_t seed, float4* wsh) {
   const double cc = u / S.pitch + 0.5 * S.W;
   const double rc = 0.5 * S.H - v / S.pitch;
   const float energy_fx = (float)(S.radiance * 2147483648.0);
@@ -154,16 +173,19 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
   const float ev1 = erff(erf_arg(S, r1 + 1, rc));
   const float mass_v = 0.5f * (ev1 - ev0);
   if (ncol <= kMaxSpot) {
-    float wu[kMaxSpot];
+    // column weights straight to shared memory, one column at a time (an
+    // unrolled erff chain held every weight in registers and spilled);
+    // columns past the window stay 0 and deposit floor(0 + u) = 0
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    wsh[0] = z4;
+    wsh[kBlock] = z4;
+    wsh[2 * kBlock] = z4;
     float e = eu0;
-#pragma unroll
-    for (int k = 0; k < kMaxSpot; ++k) {
-      wu[k] = 0.0f;  // columns past the window deposit nothing (f = floor(u) = 0)
-      if (k < ncol) {
-        const float en = erff(erf_arg(S, c0 + k + 1, cc));
-        wu[k] = 0.5f * (en - e);
-        e = en;
-      }
+#pragma unroll 1
+    for (int k = 0; k < ncol; ++k) {
+      const float en = erff(erf_arg(S, c0 + k + 1, cc));
+      reinterpret_cast<float*>(wsh + (k >> 2) * kBlock)[k & 3] = 0.5f * (en - e);
+      e = en;
     }
     const float mass_u = 0.5f * (e - eu0);
     const float scale = energy_fx / (mass_u * mass_v);
@@ -192,23 +214,27 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
         // past the window have wu = 0, so they add floor(0 + u) = 0 to a word
         // further along the tile (the allocation has kMaxSpot words of slack).
         const uint32_t trow = (uint32_t)__cvta_generic_to_shared(tile + (r - tr0) * tw + (c0 - tc0));
+        float wr[kMaxSpot];
+        lds_weights(wsh, wr, width <= 4 ? 1 : (width <= 8 ? 2 : 3));
         if (width <= 4) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint32_t f = dround(wu[k] * row_w, w);
+            const uint32_t f = dround(wr[k] * row_w, w);
             if (f) red_shared(trow + 4 * k, f);
           }
         } else if (width <= 8) {
-          red_row<8>(trow, wu, row_w, w);
+          red_row<8>(trow, wr, row_w, w);
         } else {
-          red_row<kMaxSpot>(trow, wu, row_w, w);
+          red_row<kMaxSpot>(trow, wr, row_w, w);
         }
       } else {
+        float wr[kMaxSpot];
+        lds_weights(wsh, wr, 3);
 #pragma unroll
         for (int k = 0; k < kMaxSpot; ++k) {
           const int c = c0 + k;
           if (k < ncol && c >= 0 && c < S.W) {
-            const uint32_t f = dround(wu[k] * row_w, w);
+            const uint32_t f = dround(wr[k] * row_w, w);
             if (f) add_px(S, tile, tc0, tr0, tw, th, c, r, f);
           }
         }
@@ -258,9 +284,11 @@ __device__ __forceinline__ T warp_sum(T v) {
 // GRIN loop, which keeps its instruction footprint small).
 template <bool kPair, int kField>
 __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
-                                                     : (kField == 2 ? kMinBlocksCells : kMinBlocks))
+                                                     : (kField == 2 && !kPair ? kMinBlocksCells
+                                                                              : kMinBlocks))
     render_emitters(const __grid_constant__ KScene S) {
-  extern __shared__ uint32_t tile[];
+  extern __shared__ uint32_t tile[];  // [kTileCap + kMaxSpot slack] then the deposit weights
+  float4* const wsh = reinterpret_cast<float4*>(tile + kTileCap + kMaxSpot) + threadIdx.x;
   constexpr int kWarps = kBlock / 32;
   __shared__ int sh_work, sh_src;
   __shared__ int sh_box[4];
@@ -337,19 +365,19 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
           const double3 so = make_double3(vso[0], vso[1], vso[2]);
           double3 d;
           if (emit_ray(S, ekey, so, i, d)) {
-            const RayResult r0 = finish_ray<kField>(S, so, d, false, sh_rt[tid]);
+            const RayResult r0 = finish_ray<kField>(S, so, d, false, sh_rt[tid], &sh_steps[tid]);
             sh_cnt0[r0.status][tid] += 1u;
             if (r0.status == 0) {
               sh_uv0[0][tid] += r0.u;
               sh_uv0[1][tid] += r0.v;
             }
-            r = finish_ray<kField>(S, so, d, true, sh_rt[tid]);
+            r = finish_ray<kField>(S, so, d, true, sh_rt[tid], &sh_steps[tid]);
           } else {
             r.status = 1;
-            r.steps = 0;
           }
         } else {
-          r = trace_ray<kField>(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid]);
+          r = trace_ray<kField>(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid],
+                                &sh_steps[tid]);
         }
       }
       if (k == kb && S.accumulate) {  // block-uniform branch
@@ -388,14 +416,13 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
         __syncthreads();
       }
       if (r.status >= 0) {
-        sh_steps[tid] += (unsigned long long)r.steps;
         sh_cnt[r.status][tid] += 1u;
         if (r.status == 0) {
           sh_uv[0][tid] += r.u;
           sh_uv[1][tid] += r.v;
           if (S.accumulate)
             deposit(S, r.u, r.v, tile, vtile[0], vtile[1], vtile[2], vtile[3],
-                    (uint32_t)(mix_bits(ekey + (uint64_t)i) >> 32));
+                    (uint32_t)(mix_bits(ekey + (uint64_t)i) >> 32), wsh);
         }
       }
       __syncwarp();
@@ -514,16 +541,19 @@ __global__ void trace_rays_kernel(const __grid_constant__ KScene S, int64_t n,
                                   const int64_t* __restrict__ srcs, const int32_t* __restrict__ rays,
                                   double* uv, int32_t* status, int32_t* steps) {
   __shared__ double sh_rt[128][7];
+  __shared__ unsigned long long sh_st[128];
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
+  sh_st[threadIdx.x] = 0ull;
   const int64_t src = srcs[q];
   const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
   const double3 so = make_double3(S.sources[3 * src], S.sources[3 * src + 1], S.sources[3 * src + 2]);
-  const RayResult r = trace_ray<kField>(S, mix_bits(S.key_seed + sid), so, rays[q], sh_rt[threadIdx.x]);
+  const RayResult r = trace_ray<kField>(S, mix_bits(S.key_seed + sid), so, rays[q], sh_rt[threadIdx.x],
+                                        &sh_st[threadIdx.x]);
   uv[2 * q] = r.status == 0 ? r.u : nan("");
   uv[2 * q + 1] = r.status == 0 ? r.v : nan("");
   status[q] = r.status;
-  steps[q] = r.steps;
+  steps[q] = (int32_t)sh_st[threadIdx.x];
 }
 
 // ------------------------------------------------ K0: field pack / build
@@ -620,7 +650,10 @@ __global__ void quantize_kernel(const double* __restrict__ img, int64_t n, doubl
 }
 
 // ------------------------------------------------ launch wrappers
-static size_t render_smem() { return (size_t)(kTileCap + kMaxSpot) * sizeof(uint32_t); }
+static size_t render_smem() {
+  static_assert(((kTileCap + kMaxSpot) * sizeof(uint32_t)) % 16 == 0, "weights must be 16 B aligned");
+  return (size_t)(kTileCap + kMaxSpot) * sizeof(uint32_t) + 3 * kBlock * sizeof(float4);
+}
 
 template <bool kPair, int kField>
 static void set_smem() {
@@ -628,24 +661,32 @@ static void set_smem() {
                        (int)render_smem());
 }
 
-int render_occupancy(int* blocks_per_sm, int* blocks_per_sm_no_field, int* blocks_per_sm_cells) {
+template <bool kPair, int kField>
+static int occupancy() {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, render_emitters<kPair, kField>, kBlock,
+                                                    render_smem()) != cudaSuccess)
+    return 0;
+  return n;
+}
+
+int render_occupancy(int blocks_per_sm[2][3]) {
   set_smem<false, 0>();
   set_smem<false, 1>();
   set_smem<false, 2>();
   set_smem<true, 0>();
   set_smem<true, 1>();
   set_smem<true, 2>();
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      blocks_per_sm, render_emitters<false, 1>, kBlock, render_smem());
-  if (e != cudaSuccess) return (int)e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm_cells, render_emitters<false, 2>,
-                                                    kBlock, render_smem());
-  if (e != cudaSuccess) return (int)e;
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      blocks_per_sm_no_field, render_emitters<false, 0>, kBlock, render_smem());
+  blocks_per_sm[0][0] = occupancy<false, 0>();
+  blocks_per_sm[0][1] = occupancy<false, 1>();
+  blocks_per_sm[0][2] = occupancy<false, 2>();
+  blocks_per_sm[1][0] = occupancy<true, 0>();
+  blocks_per_sm[1][1] = occupancy<true, 1>();
+  blocks_per_sm[1][2] = occupancy<true, 2>();
+  return (int)cudaGetLastError();
 }
 
-static int field_mode(const KScene& s) { return !s.with_field ? 0 : (s.cell_table ? 2 : 1); }
+int field_mode(const KScene& s) { return !s.with_field ? 0 : (s.cell_table ? 2 : 1); }
 
 cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream) {
   const size_t sm = render_smem();

@@ -22,7 +22,7 @@ constexpr int kMinBlocks = RB_MINB;  // resident CTAs per SM the register budget
 #endif
 constexpr int kMinBlocksNoField = RB_MINB_NOFIELD;  // the same for scenes without a medium
 #ifndef RB_MINB_CELLS
-#define RB_MINB_CELLS 3  // cell-table GRIN loop fits 80 registers: bos +3.5%, 1024^3 +5%
+#define RB_MINB_CELLS 3  // cell-table GRIN loop fits 80 registers: bos +3.5%, 1024^3 +5% (not pair mode)
 #endif
 constexpr int kMinBlocksCells = RB_MINB_CELLS;  // ... and for fields read from the cell table
 constexpr int kTileCap = 6144;       // u32 entries of the per-emitter shared tile (24 KB)
@@ -151,7 +151,9 @@ cudaError_t launch_build_fp64(const float* rho, int nx, int ny, int nz, double k
                               double* n, double* gx, double* gy, double* gz, cudaStream_t stream);
 cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream);
 cudaError_t launch_emitter_stats(const KScene& s, cudaStream_t stream);
-int render_occupancy(int* blocks_per_sm, int* blocks_per_sm_no_field, int* blocks_per_sm_cells);
+// resident CTAs per SM of each render_emitters instantiation, [pair][field mode]
+int render_occupancy(int blocks_per_sm[2][3]);
+int field_mode(const KScene& s);  // 0 no medium, 1 nodes, 2 cell table
 cudaError_t launch_trace_rays(const KScene& s, int64_t n, const int64_t* src, const int32_t* ray,
                               double* uv, int32_t* status, int32_t* steps, cudaStream_t stream);
 cudaError_t launch_pack_nodes(const double* n, const double* gx, const double* gy,

@@ -8,8 +8,11 @@ timeout 1200 python bench.py > $O/bench_tomo.json 2> $O/bench_tomo.err; echo "be
 for s in bos piv optics; do
   timeout 900 python bench.py --scene $s --steps 3 --warmup 3 > $O/bench_$s.json 2> $O/bench_$s.err; echo "bench $s rc=$?"
 done
+timeout 1200 python bench.py --scene large --scale 0.125 --steps 3 --warmup 3 > $O/bench_large.json 2> $O/bench_large.err; echo "bench large rc=$?"
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref_tomo.json 2> $O/bench_ref.err; echo "ref rc=$?"
 L="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 $L > $O/launch_plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $L > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 F="python scripts/run_scene.py tomo 1.0"
 $F > $O/full_plain.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:render_emitters -s 1 -c 1 -o $O/prof_k1_tomo $F > $O/ncu_full.log 2>&1; echo "ncu full rc=$?"
+B="python scripts/run_scene.py bos 1.0"
+$B > $O/bos_plain.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:render_emitters -s 1 -c 1 -o $O/prof_k1_bos $B > $O/ncu_bos.log 2>&1; echo "ncu bos rc=$?"
