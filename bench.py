@@ -296,7 +296,7 @@ def main_ours(args, rank, world, local):
     sampler.start()
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    total_ms, kernel_ms, steps_sum, rays_local = 0.0, [], 0, 0
+    total_ms, kernel_ms, steps_sum, rays_local, launches = 0.0, [], 0, 0, 0
     for k in range(args.steps):
         flush.fill_(k & 0xFF)
         barrier()
@@ -306,6 +306,7 @@ def main_ours(args, rank, world, local):
         torch.cuda.synchronize()
         total_ms += ev0.elapsed_time(ev1)
         kernel_ms.append(rep["kernel_ms"])
+        launches += rep["kernel_launches"]  # render + split-stats kernels (library count)
         steps_sum = rep["total_steps"]
         rays_local = rep["emitted"]
     clocks = sampler.stop()
@@ -389,7 +390,7 @@ def main_ours(args, rank, world, local):
             "config": dict(workload_config(args, scene, desc, info, world),
                            field_upload_s=field_s, steps_per_ray=steps_sum / max(rays_local, 1)),
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-            "gpu_launches": args.steps}
+            "gpu_launches": launches}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -168,7 +168,7 @@ typedef struct rb_trace_out {
   uint16_t* quantized;
   double gain;
   int32_t bit_depth;
-  int32_t reserved2;
+  int32_t kernel_launches; /* out: CUDA kernels this call launched (all devices) */
 } rb_trace_out;
 
 typedef struct rb_ctx rb_ctx;

@@ -65,7 +65,7 @@ class TraceOut(C.Structure):
                 ("wall_seconds", C.c_double), ("threads", C.c_int32), ("reserved", C.c_int32),
                 ("config_hash", C.c_uint64), ("total_steps", C.c_int64),
                 ("kernel_ms", C.c_double), ("quantized", C.POINTER(C.c_uint16)),
-                ("gain", C.c_double), ("bit_depth", C.c_int32), ("reserved2", C.c_int32)]
+                ("gain", C.c_double), ("bit_depth", C.c_int32), ("kernel_launches", C.c_int32)]
 
 
 def vec3(v) -> Vec3:

@@ -331,6 +331,7 @@ struct PartialOut {
   unsigned long long counters0[6] = {0, 0, 0, 0, 0, 0};
   float ms = 0.f;
   int err_flag = 0;
+  int launches = 0;  // kernels render_on launched
 };
 
 // CTAs per emitter (KScene::split).  Splitting an emitter's rays over several
@@ -443,9 +444,11 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
       1, std::min<int64_t>(dev.sms * dev.blocks_per_sm[k.pair ? 1 : 0][rbk::field_mode(k)],
                            std::max<int64_t>(1, units))));
   RB_CUDA(ctx, cudaEventRecord(dev.ev0, st));
+  po.launches = 0;
   if (!work.empty()) {
     RB_CUDA(ctx, rbk::launch_render(k, grid, st));
     RB_CUDA(ctx, rbk::launch_emitter_stats(k, st));
+    po.launches = 1 + (k.split > 1 && k.n_work > 0 ? 1 : 0);
   }
   RB_CUDA(ctx, cudaEventRecord(dev.ev1, st));
   po.hit.assign(2 * n, 0.0);
@@ -905,6 +908,7 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
   const int nd = static_cast<int>(ctx->devs.size());
   out->threads = nd;
   out->kernel_ms = 0.0;
+  out->kernel_launches = 0;
   if (s->n_sources == 0) {  // engine.cpp:436: one "thread", blank image, no stats
     if (accumulate_image && out->image) std::memset(out->image, 0, npx * sizeof(double));
     if (accumulate_image && out->quantized) std::memset(out->quantized, 0, npx * sizeof(uint16_t));
@@ -944,9 +948,11 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
   unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
   int64_t landed_total = 0;
   float ms = 0.f;
+  int launches = 0;
   for (int d = 0; d < used; ++d) {
     for (int j = 0; j < 6; ++j) c[j] += parts[d].counters[j];
     ms = std::max(ms, parts[d].ms);
+    launches += parts[d].launches;
     for (int32_t src : work[d]) {
       if (out->hit_sum) {
         out->hit_sum[2 * src] = parts[d].hit[2 * src];
@@ -981,6 +987,7 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
     RB_CUDA(ctx, rbk::launch_image_finalize(d0.image.as<unsigned long long>(),
                                             d0.dimage.as<double>(), static_cast<int64_t>(npx),
                                             d0.stream));
+    ++launches;
     RB_CUDA(ctx, cudaMemcpyAsync(out->image, d0.dimage.p, npx * sizeof(double),
                                  cudaMemcpyDeviceToHost, d0.stream));
     if (out->quantized) {  // render's quantize on device (sensor.cpp:124-135)
@@ -988,6 +995,7 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
       RB_CUDA(ctx, rbk::launch_quantize(d0.dimage.as<double>(), static_cast<int64_t>(npx),
                                         out->gain, out->bit_depth, d0.qimage.as<uint16_t>(),
                                         d0.stream));
+      ++launches;
       RB_CUDA(ctx, cudaMemcpyAsync(out->quantized, d0.qimage.p, npx * sizeof(uint16_t),
                                    cudaMemcpyDeviceToHost, d0.stream));
     }
@@ -996,6 +1004,7 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
   fill_report(out, s, s->n_sources, c, landed_total);
   out->threads = used;
   out->kernel_ms = ms;
+  out->kernel_launches = launches;
   out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return RB_OK;
 }
@@ -1033,6 +1042,7 @@ int rb_trace_shard(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulat
   }
   fill_report(out, s, static_cast<int64_t>(work.size()), po.counters, landed_total);
   out->kernel_ms = po.ms;
+  out->kernel_launches = po.launches;
   out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return RB_OK;
 }
@@ -1359,6 +1369,9 @@ extern "C" int rb_trace_bos_pair(rb_ctx* ctx, const rb_scene* s, rb_trace_out* o
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   out_ref->threads = out_grad->threads = used;
   out_ref->kernel_ms = out_grad->kernel_ms = ms;
+  int launches = 0;
+  for (int d = 0; d < used; ++d) launches += parts[d].launches;
+  out_ref->kernel_launches = out_grad->kernel_launches = launches;
   out_ref->wall_seconds = out_grad->wall_seconds = wall;
   return RB_OK;
 }

@@ -113,10 +113,22 @@ def test_emitter_split_is_invisible(tracer, name, monkeypatch):
         r, p = runs[split]
         assert np.array_equal(r.image, r1.image)
         assert np.array_equal(r.landed, r1.landed)
-        drop = ("kernel_ms", "wall_seconds")
+        drop = ("kernel_ms", "wall_seconds", "kernel_launches")
         assert {k: v for k, v in r.report.items() if k not in drop} == \
             {k: v for k, v in r1.report.items() if k not in drop}
         np.testing.assert_allclose(r.hit_sum, r1.hit_sum, rtol=1e-12, atol=1e-15)
         for a, b in zip(p, p1):
             assert np.array_equal(a.landed, b.landed)
             np.testing.assert_allclose(a.hit_sum, b.hit_sum, rtol=1e-12, atol=1e-15)
+
+
+def test_kernel_launch_count_is_reported(tracer, monkeypatch):
+    """rb_trace_out.kernel_launches: render (+ the chunk-stats kernel when
+    emitters are split) (+ image finalize for rb_trace)."""
+    scene, field, g = load("shock_particles")
+    tracer.set_field(field)
+    monkeypatch.setenv("RAYBOS_SPLIT", "1")
+    assert tracer.run_trace(scene, True, True).report["kernel_launches"] == 2
+    assert tracer.run_trace(scene, True, False).report["kernel_launches"] == 1
+    monkeypatch.setenv("RAYBOS_SPLIT", "4")
+    assert tracer.run_trace(scene, True, True).report["kernel_launches"] == 3
