@@ -17,6 +17,10 @@
 // vector helpers and the status enums.
 #pragma once
 
+#ifndef RB_UNIFORM_RELOAD
+#define RB_UNIFORM_RELOAD 0  // see sample_d_poly
+#endif
+
 
 // Grid geometry, read straight from the kernel parameters (constant bank) so
 // it occupies no registers in the RK4 loop.
@@ -25,79 +29,12 @@ struct GridView {
   __device__ __forceinline__ explicit GridView(const KScene& s) : S(s) {}
 };
 
-// D = n grad(n) at grid coordinates (qx, qy, qz): trilinear interpolation of
-// the float4 nodes (n-1, dn/dx, dn/dy, dn/dz) with the point clamped to the box
-// first.  Index clamp: the unsigned conversion saturates negatives to cell 0;
-// the fraction is saturated to [0, 1], which together equal clamping q.
-__device__ __forceinline__ float3 sample_d(const GridView& G, float qx, float qy, float qz) {
-  const unsigned i = min(__float2uint_rz(qx), G.S.g_ix);
-  const unsigned j = min(__float2uint_rz(qy), G.S.g_iy);
-  const unsigned k = min(__float2uint_rz(qz), G.S.g_iz);
-  const float fx = __saturatef(qx - (float)i);
-  const float fy = __saturatef(qy - (float)j);
-  const float fz = __saturatef(qz - (float)k);
-  const float4* p0 = G.S.grid + (k * G.S.g_nxny + j * G.S.g_nx + i);
-  const float4* p1 = p0 + G.S.g_nxny;
-  const float4 c000 = __ldg(p0), c100 = __ldg(p0 + 1);
-  const float4 c010 = __ldg(p0 + G.S.g_nx), c110 = __ldg(p0 + G.S.g_nx + 1);
-  const float4 c001 = __ldg(p1), c101 = __ldg(p1 + 1);
-  const float4 c011 = __ldg(p1 + G.S.g_nx), c111 = __ldg(p1 + G.S.g_nx + 1);
-  const float gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
-  const float w00 = gx * gy, w10 = fx * gy, w01 = gx * fy, w11 = fx * fy;
-  const float w000 = w00 * gz, w100 = w10 * gz, w010 = w01 * gz, w110 = w11 * gz;
-  const float w001 = w00 * fz, w101 = w10 * fz, w011 = w01 * fz, w111 = w11 * fz;
-#define RB_LERP(ch)                                                                         \
-  (w000 * c000.ch + w100 * c100.ch + w010 * c010.ch + w110 * c110.ch + w001 * c001.ch +    \
-   w101 * c101.ch + w011 * c011.ch + w111 * c111.ch)
-  const float n = 1.0f + RB_LERP(x);
-  return make_float3(RB_LERP(y) * n, RB_LERP(z) * n, RB_LERP(w) * n);
-#undef RB_LERP
-}
-
-// The same sample with the 8 corners of the last cell kept in registers: a step
-// advances the ray by about half a cell and its three RK stages lie within
-// that half cell, so most samples reuse the cached corners and skip the eight
-// 16-byte gathers (whose L1 -> register writeback, 384 B per ray-step, is the
-// roof of the uncached loop).
-struct CellCache {
-  unsigned key;  // linear index of the cached cell's (0,0,0) corner, ~0u = empty
-  float4 c000, c100, c010, c110, c001, c101, c011, c111;
-};
-
-__device__ __forceinline__ float3 sample_d_cached(const GridView& G, CellCache& C, float qx,
-                                                  float qy, float qz) {
-  const unsigned i = min(__float2uint_rz(qx), G.S.g_ix);
-  const unsigned j = min(__float2uint_rz(qy), G.S.g_iy);
-  const unsigned k = min(__float2uint_rz(qz), G.S.g_iz);
-  const float fx = __saturatef(qx - (float)i);
-  const float fy = __saturatef(qy - (float)j);
-  const float fz = __saturatef(qz - (float)k);
-  const unsigned key = k * G.S.g_nxny + j * G.S.g_nx + i;
-  if (key != C.key) {
-    C.key = key;
-    const float4* p0 = G.S.grid + key;
-    const float4* p1 = p0 + G.S.g_nxny;
-    C.c000 = __ldg(p0);
-    C.c100 = __ldg(p0 + 1);
-    C.c010 = __ldg(p0 + G.S.g_nx);
-    C.c110 = __ldg(p0 + G.S.g_nx + 1);
-    C.c001 = __ldg(p1);
-    C.c101 = __ldg(p1 + 1);
-    C.c011 = __ldg(p1 + G.S.g_nx);
-    C.c111 = __ldg(p1 + G.S.g_nx + 1);
-  }
-  const float gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
-  const float w00 = gx * gy, w10 = fx * gy, w01 = gx * fy, w11 = fx * fy;
-  const float w000 = w00 * gz, w100 = w10 * gz, w010 = w01 * gz, w110 = w11 * gz;
-  const float w001 = w00 * fz, w101 = w10 * fz, w011 = w01 * fz, w111 = w11 * fz;
-#define RB_LERP(ch)                                                                            \
-  (w000 * C.c000.ch + w100 * C.c100.ch + w010 * C.c010.ch + w110 * C.c110.ch +                \
-   w001 * C.c001.ch + w101 * C.c101.ch + w011 * C.c011.ch + w111 * C.c111.ch)
-  const float n = 1.0f + RB_LERP(x);
-  return make_float3(RB_LERP(y) * n, RB_LERP(z) * n, RB_LERP(w) * n);
-#undef RB_LERP
-}
-
+// D = n grad(n) at grid coordinates q: the trilinear interpolation of the float4
+// nodes (n-1, dn/dx, dn/dy, dn/dz) of GriddedField::sample (scene.cpp:99-135)
+// with the point clamped to the box first (ClampedD, grin.cpp:23-33).  Index
+// clamp: the unsigned conversion saturates negatives to cell 0; the fraction
+// is saturated to [0, 1], which together equal clamping q.
+//
 // Cached cell in polynomial form.  On a cell change the 8 corners are loaded
 // once and turned into the coefficients of
 //   v(fx,fy,fz) = a + b fx + c fy + d fz + e fx fy + f fx fz + g fy fz + h fx fy fz
@@ -186,9 +123,9 @@ __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, 
   // fast path: inside the cached cell (NaN fails and takes the full path)
   const bool stay = fminf(fminf(fx, fy), fz) >= 0.0f && fmaxf(fmaxf(fx, fy), fz) <= 1.0f;
 #if RB_UNIFORM_RELOAD
-  // Warp-uniform reload: when any active lane leaves its cell, all active lanes
-  // take the reload path (lanes still inside re-derive the same cell), so the
-  // branch needs no divergence bookkeeping.
+  // Warp-uniform variant: when any active lane leaves its cell all active lanes
+  // take the reload path.  Measured equal to the per-lane branch (the 32 rays
+  // of a compact pupil patch cross cell faces together), so it is off.
   const bool reload = __any_sync(__activemask(), !stay);
 #else
   const bool reload = !stay;
@@ -197,19 +134,7 @@ __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, 
   return poly_eval(P, fx, fy, fz);
 }
 
-#ifndef RB_UNIFORM_RELOAD
-#define RB_UNIFORM_RELOAD 1
-#endif
-#ifndef RB_CELL_CACHE
-#define RB_CELL_CACHE 2
-#endif
-#if RB_CELL_CACHE == 2
 #define RB_SAMPLE_D(qx, qy, qz) sample_d_poly<kCells>(G, cache, qx, qy, qz)
-#elif RB_CELL_CACHE == 1
-#define RB_SAMPLE_D(qx, qy, qz) sample_d_cached(G, cache, qx, qy, qz)
-#else
-#define RB_SAMPLE_D(qx, qy, qz) sample_d(G, qx, qy, qz)
-#endif
 
 __device__ __forceinline__ float sample_nm1(const GridView& G, float qx, float qy, float qz) {
   const unsigned i = min(__float2uint_rz(qx), G.S.g_ix);
@@ -292,13 +217,8 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
 
   float drx = 0.f, dry = 0.f, drz = 0.f, dtx = 0.f, dty = 0.f, dtz = 0.f;
   float pax = q0x, pay = q0y, paz = q0z;  // unperturbed line at xi = step * h
-#if RB_CELL_CACHE == 2
   CellPoly cache;
   cache.ox = cache.oy = cache.oz = -1e30f;
-#elif RB_CELL_CACHE == 1
-  CellCache cache;
-  cache.key = ~0u;
-#endif
   const int max_steps = S.max_steps;
 #ifndef RB_STEP_UNROLL
 #define RB_STEP_UNROLL 1

@@ -26,7 +26,7 @@ for blk, mb, cc, uu, dd, sp, ur in variants:
     tag = os.environ.get("TAG", "")
     obj = os.path.join(OUT, f"k_{blk}_{mb}_c{cc}_u{uu}_d{dd}_s{sp}_r{ur}{tag}.o")
     subprocess.run([NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", *ARCH,
-                    f"-DRB_BLOCK={blk}", f"-DRB_MINB={mb}", f"-DRB_CELL_CACHE={cc}", f"-DRB_UNIFORM_RELOAD={uu}", f"-DRB_DITHER={dd}", f"-DRB_SPECULATE={sp}", f"-DRB_STEP_UNROLL={ur}", *os.environ.get("EXTRA", "").split(), f"-I{ROOT}/include", "-c",
+                    f"-DRB_BLOCK={blk}", f"-DRB_MINB={mb}", f"-DRB_UNIFORM_RELOAD={uu}", f"-DRB_DITHER={dd}", f"-DRB_STEP_UNROLL={ur}", *os.environ.get("EXTRA", "").split(), f"-I{ROOT}/include", "-c",
                     os.path.join(PKG, "csrc", "kernels.cu"), "-o", obj], check=True)
     lib = os.path.join(OUT, f"libraybos_gpu_{blk}_{mb}_c{cc}_u{uu}_d{dd}_s{sp}_r{ur}{tag}.so")
     subprocess.run([NVCC, "-shared", *ARCH, capi, fp64, obj, "-o", lib, "-ldl", "-lpthread"], check=True)
