@@ -208,8 +208,9 @@ rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, in
   k.sampling = s->sampling == RB_SAMPLING_STRATIFIED ? 0 : 1;
   {
     const int rows = (s->rays_per_source + k.cells - 1) / k.cells;
-    k.patch_px = (k.cells + 7) / 8;
-    k.patch_count = k.patch_px * ((rows + 3) / 4);
+    k.band_rays = 4 * k.cells;
+    const int64_t band_positions = static_cast<int64_t>((rows + 3) / 4) * k.band_rays;
+    k.patch_count = static_cast<int32_t>((band_positions + 31) / 32);
     const int warps = rbk::kBlock / 32;
     int st = std::max(1, k.patch_count / warps);
     while (std::gcd(st, k.patch_count) != 1) ++st;

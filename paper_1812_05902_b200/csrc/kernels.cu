@@ -353,9 +353,10 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
       const int slot = k * kWarps + warp;
       if (slot < S.patch_count) {
         const int p = (int)(((long long)slot * S.patch_stride) % S.patch_count);
-        const int py = p / S.patch_px, px = p - py * S.patch_px;
-        const int cx = px * 8 + (lane & 7), cy = py * 4 + (lane >> 3);
-        if (cx < S.cells && cy * S.cells + cx < N) i = cy * S.cells + cx;
+        const int j = p * 32 + lane;  // position in the 4-row bands (kernels.h)
+        const int band = j / S.band_rays, rem = j - band * S.band_rays;
+        const int cx = rem >> 2, cy = band * 4 + (rem & 3);
+        if (cy * S.cells + cx < N) i = cy * S.cells + cx;
       }
       const uint64_t ekey = *vkey;
       RayResult r;

@@ -72,11 +72,13 @@ struct KScene {
   int32_t cells;                 // ceil(sqrt(N))
   int32_t sampling;
   int32_t with_field;
-  // warp patches: each warp-iteration traces a compact 8x4 block of the pupil
-  // lattice (cells x rows, ray i = cy * cells + cx) so its 32 rays gather from
-  // the same few grid cells; patches are visited in a strided order so the
-  // first iteration (the tile pilot) samples the whole pupil.
-  int32_t patch_px;              // patches per lattice row (ceil(cells / 8))
+  // warp patches: the pupil lattice (cells x rows, ray i = cy * cells + cx) is
+  // cut into bands of 4 rows, each enumerated column-major, so 32 consecutive
+  // band positions are a compact 8x4 block whose rays gather from the same
+  // few grid cells, and no lane idles where cells is not a multiple of 8 (only
+  // the warps that straddle two bands are split); patches are visited in a
+  // strided order so the first iteration (the tile pilot) samples the whole pupil.
+  int32_t band_rays;             // 4 * cells
   int32_t patch_count;
   int32_t patch_stride;          // coprime to patch_count
   int32_t pad_patch;
