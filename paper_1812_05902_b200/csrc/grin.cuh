@@ -107,13 +107,59 @@ __device__ __forceinline__ void poly_load(const GridView& G, CellPoly& P, float 
                     P.g, P.h);
 }
 
+#ifndef RB_FFMA2
+#define RB_FFMA2 1
+#endif
+// Packed FP32 pairs (sm_100 FFMA2 / FMUL2: two lanes per instruction, each
+// rounded exactly like fmaf / a single multiply, so results are bit-identical
+// to the scalar form).  A scalar operand packed as {s, s} becomes the
+// instruction's broadcast (.F32) operand.
+__device__ __forceinline__ unsigned long long f2pk(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2up(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(float s, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2pk(s, s)), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fmul2(float s, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2pk(s, s)), "l"(b));
+  return d;
+}
+
 __device__ __forceinline__ float3 poly_eval(const CellPoly& P, float fx, float fy, float fz) {
+#if RB_FFMA2
+  // the same Horner tree as below, channels (x, y) and (z, w) in pairs
+#define RB_HORNER2(lo, hi)                                                                      \
+  ffma2(fx,                                                                                     \
+        ffma2(fz, f2pk(P.f.lo, P.f.hi),                                                         \
+              ffma2(fy, ffma2(fz, f2pk(P.h.lo, P.h.hi), f2pk(P.e.lo, P.e.hi)),                   \
+                    f2pk(P.b.lo, P.b.hi))),                                                     \
+        ffma2(fy, ffma2(fz, f2pk(P.g.lo, P.g.hi), f2pk(P.c.lo, P.c.hi)),                        \
+              ffma2(fz, f2pk(P.d.lo, P.d.hi), f2pk(P.a.lo, P.a.hi))))
+  const float2 xy = f2up(RB_HORNER2(x, y));
+  const unsigned long long zw = RB_HORNER2(z, w);
+#undef RB_HORNER2
+  const float n = 1.0f + xy.x;
+  const float2 nzw = f2up(fmul2(n, zw));
+  return make_float3(xy.y * n, nzw.x, nzw.y);
+#else
 #define RB_HORNER(ch)                                                                         \
   fmaf(fx, fmaf(fz, P.f.ch, fmaf(fy, fmaf(fz, P.h.ch, P.e.ch), P.b.ch)),                     \
        fmaf(fy, fmaf(fz, P.g.ch, P.c.ch), fmaf(fz, P.d.ch, P.a.ch)))
   const float n = 1.0f + RB_HORNER(x);
   return make_float3(RB_HORNER(y) * n, RB_HORNER(z) * n, RB_HORNER(w) * n);
 #undef RB_HORNER
+#endif
 }
 
 template <bool kCells>
@@ -188,7 +234,7 @@ __device__ __forceinline__ bool aabb_intersect(const KScene& S, double3 o, doubl
 // there during the RK4 loop (they are only needed again at the exit).
 template <bool kCells>
 __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& d,
-                                          unsigned long long* steps_acc,
+                                          unsigned* steps_acc,
                                           double* scratch) {
   double tn;
   if (!aabb_intersect(S, o, d, tn)) return kMissed;
@@ -300,7 +346,9 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
     status = kTraced;
     break;
   }
-  *steps_acc += (unsigned long long)(step + (status == kTraced ? 1 : 0));  // kLost: step == max_steps
+  // 32-bit on purpose: a 64-bit add of the exit count made the optimiser widen
+  // the loop counter itself to 64 bits (and spill its high word every step)
+  *steps_acc += (unsigned)(step + (status == kTraced ? 1 : 0));  // kLost: step == max_steps
   return status;
 }
 

@@ -44,10 +44,11 @@ __device__ __forceinline__ bool emit_ray(const KScene& S, uint64_t ekey, double3
 // Stages 2-4 of process_source (engine.cpp:112-137) for an emitted ray.
 // kField: 0 = the scene has no medium (no GRIN code at all), 1 = field read
 // from the float4 nodes, 2 = from the per-cell coefficient table.
-// The ray's RK4 steps are added to *steps_acc.
+// The ray's RK4 steps are added to *steps_acc (a per-thread shared counter,
+// folded into the 64-bit per-unit count after every ray).
 template <int kField>
 __device__ __forceinline__ RayResult finish_ray(const KScene& S, double3 o, double3 d, bool field,
-                                                double* scratch, unsigned long long* steps_acc) {
+                                                double* scratch, unsigned* steps_acc) {
   RayResult r;
   r.u = r.v = 0.0;
   if (kField != 0 && field) {
@@ -73,7 +74,7 @@ __device__ __forceinline__ RayResult finish_ray(const KScene& S, double3 o, doub
 // process_source's per-ray body, engine.cpp:112-137.
 template <int kField>
 __device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, double3 src, int i,
-                                               double* scratch, unsigned long long* steps_acc) {
+                                               double* scratch, unsigned* steps_acc) {
   double3 d;
   if (!emit_ray(S, ekey, src, i, d)) {
     RayResult r;
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
   __shared__ double sh_uv[2][kBlock];
   __shared__ unsigned sh_cnt[6][kBlock];     // landed, lost, aperture, miss, tir, smiss
   __shared__ unsigned long long sh_steps[kBlock];  // RK4 steps (64-bit: rays x max_steps)
+  __shared__ unsigned sh_st32[kBlock];             // the ray in flight's steps
   __shared__ double sh_rt[kBlock][7];        // R0, T0 of the ray in flight (grin.cuh)
   __shared__ double sh_d[2][kWarps];
   __shared__ unsigned long long sh_l[7][kWarps];
@@ -341,6 +343,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
 #pragma unroll
     for (int j = 0; j < 7; ++j) sh_cnt0[j][tid] = 0u;
     sh_steps[tid] = 0ull;
+    sh_st32[tid] = 0u;
     __syncthreads();
     if (sh_work >= n_units) break;
     const int kb = (sh_work % S.split) * Kc, ke = min(K, kb + Kc);
@@ -366,20 +369,22 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
           const double3 so = make_double3(vso[0], vso[1], vso[2]);
           double3 d;
           if (emit_ray(S, ekey, so, i, d)) {
-            const RayResult r0 = finish_ray<kField>(S, so, d, false, sh_rt[tid], &sh_steps[tid]);
+            const RayResult r0 = finish_ray<kField>(S, so, d, false, sh_rt[tid], &sh_st32[tid]);
             sh_cnt0[r0.status][tid] += 1u;
             if (r0.status == 0) {
               sh_uv0[0][tid] += r0.u;
               sh_uv0[1][tid] += r0.v;
             }
-            r = finish_ray<kField>(S, so, d, true, sh_rt[tid], &sh_steps[tid]);
+            r = finish_ray<kField>(S, so, d, true, sh_rt[tid], &sh_st32[tid]);
           } else {
             r.status = 1;
           }
         } else {
           r = trace_ray<kField>(S, ekey, make_double3(vso[0], vso[1], vso[2]), i, sh_rt[tid],
-                                &sh_steps[tid]);
+                                &sh_st32[tid]);
         }
+        sh_steps[tid] += sh_st32[tid];
+        sh_st32[tid] = 0u;
       }
       if (k == kb && S.accumulate) {  // block-uniform branch
         if (r.status == 0) {  // spot_pixel_window of the pilot, clipped to the frame
@@ -542,10 +547,10 @@ __global__ void trace_rays_kernel(const __grid_constant__ KScene S, int64_t n,
                                   const int64_t* __restrict__ srcs, const int32_t* __restrict__ rays,
                                   double* uv, int32_t* status, int32_t* steps) {
   __shared__ double sh_rt[128][7];
-  __shared__ unsigned long long sh_st[128];
+  __shared__ unsigned sh_st[128];
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
-  sh_st[threadIdx.x] = 0ull;
+  sh_st[threadIdx.x] = 0u;
   const int64_t src = srcs[q];
   const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
   const double3 so = make_double3(S.sources[3 * src], S.sources[3 * src + 1], S.sources[3 * src + 2]);
