@@ -111,7 +111,9 @@ def measure_peaks(device: int) -> dict:
     lib.rbp_l2_gather_gbs.argtypes = [C.c_int, C.c_double]
     reg = lib.rbp_ffma_tflops(device, 0)
     imm = lib.rbp_ffma_tflops(device, 1)
-    return {"ffma_reg_tflops": reg, "ffma_imm_tflops": imm, "ffma_tflops": max(reg, imm),
+    pk2 = lib.rbp_ffma_tflops(device, 2)   # packed FFMA2, which K1's Horner evaluation uses
+    return {"ffma_reg_tflops": reg, "ffma_imm_tflops": imm, "ffma2_tflops": pk2,
+            "ffma_tflops": max(reg, imm, pk2),
             "l2_gather_gbs": lib.rbp_l2_gather_gbs(device, 64.0)}
 
 
@@ -365,7 +367,7 @@ def main_ours(args, rank, world, local):
                 "traffic_source": "profiles/k1_traffic.json (ncu --set full, one launch)",
                 "kernel": "render_emitters", "kernel_ms": kms,
                 "peak_source": "measured on this box: FFMA microbenchmark (tools/peaks.cu), "
-                               "max of register/immediate operand forms",
+                               "max of register / immediate / packed-FFMA2 forms",
                 "per_ray": f"{FLOPS_PER_STEP:.0f} flops/RK4 step + {FLOPS_PER_RAY:.0f}; "
                            f"{steps_sum / max(rays_local, 1):.1f} steps/ray measured",
                 # what the samples would move if each gathered its 8 corners
@@ -375,7 +377,8 @@ def main_ours(args, rank, world, local):
                            "l2_gather_peak_gbs": peaks["l2_gather_gbs"],
                            "bytes_per_step": GATHER_BYTES_PER_STEP},
                 "ffma_reg_tflops": peaks["ffma_reg_tflops"],
-                "ffma_imm_tflops": peaks["ffma_imm_tflops"], "hbm_gbs_measured": measured_hbm()}
+                "ffma_imm_tflops": peaks["ffma_imm_tflops"],
+                "ffma2_tflops": peaks["ffma2_tflops"], "hbm_gbs_measured": measured_hbm()}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:

@@ -30,6 +30,25 @@ __global__ void __launch_bounds__(256) ffma_kernel(float* out, float b, float c,
   if (s == 12345.678f) out[threadIdx.x] = s;
 }
 
+// Packed FP32 pairs (FFMA2, sm_100): 8 independent pairs = 16 FMAs per step.
+__global__ void __launch_bounds__(256) ffma2_kernel(float* out, float b, float c, int iters) {
+  unsigned long long a[8];
+  const unsigned long long bb = ((unsigned long long)__float_as_uint(b) << 32) | __float_as_uint(b);
+  const unsigned long long cc = ((unsigned long long)__float_as_uint(c) << 32) | __float_as_uint(c);
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    a[j] = ((unsigned long long)__float_as_uint(threadIdx.x * 1e-3f + j) << 32) |
+           __float_as_uint(threadIdx.x * 2e-3f + j);
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[j]) : "l"(bb), "l"(cc));
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += __uint_as_float((unsigned)a[j]) + __uint_as_float((unsigned)(a[j] >> 32));
+  if (s == 12345.678f) out[threadIdx.x] = s;
+}
+
 __global__ void __launch_bounds__(256) gather_kernel(const float4* __restrict__ p, size_t n,
                                                      int reps, float* out) {
   float acc = 0.f;
@@ -47,7 +66,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const float4* __restrict__ 
 extern "C" {
 
 // Best-of-5 FP32 FFMA throughput in TFLOP/s (2 flops per FMA).  mode 0:
-// register operands, 1: immediate operands.
+// register operands, 1: immediate operands, 2: packed pairs (FFMA2).
 double rbp_ffma_tflops(int device, int mode) {
   cudaSetDevice(device);
   int sms = 0;
@@ -61,13 +80,14 @@ double rbp_ffma_tflops(int device, int mode) {
   double best = 0.0;
   for (int rep = 0; rep < 6; ++rep) {
     cudaEventRecord(e0);
-    if (mode) ffma_kernel<true><<<blocks, threads>>>(out, 0.999f, 1e-3f, iters);
+    if (mode == 2) ffma2_kernel<<<blocks, threads>>>(out, 0.999f, 1e-3f, iters);
+    else if (mode) ffma_kernel<true><<<blocks, threads>>>(out, 0.999f, 1e-3f, iters);
     else ffma_kernel<false><<<blocks, threads>>>(out, 0.999f, 1e-3f, iters);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
-    const double flops = 2.0 * 8.0 * iters * (double)blocks * threads;
+    const double flops = 2.0 * (mode == 2 ? 16.0 : 8.0) * iters * (double)blocks * threads;
     if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
   }
   cudaEventDestroy(e0);
