@@ -611,28 +611,34 @@ __global__ void build_from_density_kernel(const float* __restrict__ rho, int nx,
 }
 
 // Per-cell coefficient table (KScene::cell_table) from the packed nodes.
-__global__ void build_cells_kernel(const float4* __restrict__ grid, int nx, int ny, int nz,
-                                   CellCoef* __restrict__ cells) {
+// Each thread derives one cell's 8 coefficients; the block stages its 256
+// cells (32 KB) in shared memory and writes them out as consecutive float4 so
+// every store instruction covers 4 KB of contiguous table (direct 128 B-per-
+// thread stores ran at 1.65 TB/s).
+constexpr int kCellsPerBlock = 256;
+__global__ void __launch_bounds__(kCellsPerBlock)
+    build_cells_kernel(const float4* __restrict__ grid, int nx, int ny, int nz,
+                       CellCoef* __restrict__ cells) {
+  __shared__ float4 stage[kCellsPerBlock * 8];
   const int64_t cx = nx - 1, cxy = (int64_t)(nx - 1) * (ny - 1);
   const int64_t count = cxy * (nz - 1);
   const int64_t nxny = (int64_t)nx * ny;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = t / cxy, rem = t - k * cxy, j = rem / cx, i = rem - j * cx;
-    const float4* p0 = grid + (k * nxny + j * nx + i);
-    const float4* p1 = p0 + nxny;
-    float4 a, b, c, d, e, f, g, h;
-    cell_coefficients(p0[0], p0[1], p0[nx], p0[nx + 1], p1[0], p1[1], p1[nx], p1[nx + 1], a, b, c,
-                      d, e, f, g, h);
-    float4* o = cells[t].c;
-    o[0] = a;
-    o[1] = b;
-    o[2] = c;
-    o[3] = d;
-    o[4] = e;
-    o[5] = f;
-    o[6] = g;
-    o[7] = h;
+  for (int64_t base = (int64_t)blockIdx.x * kCellsPerBlock; base < count;
+       base += (int64_t)gridDim.x * kCellsPerBlock) {
+    const int64_t t = base + threadIdx.x;
+    if (t < count) {
+      const int64_t k = t / cxy, rem = t - k * cxy, j = rem / cx, i = rem - j * cx;
+      const float4* p0 = grid + (k * nxny + j * nx + i);
+      const float4* p1 = p0 + nxny;
+      float4* o = stage + threadIdx.x * 8;
+      cell_coefficients(p0[0], p0[1], p0[nx], p0[nx + 1], p1[0], p1[1], p1[nx], p1[nx + 1], o[0],
+                        o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+    }
+    __syncthreads();
+    const int64_t n = min((int64_t)kCellsPerBlock, count - base) * 8;
+    float4* dst = cells[base].c;
+    for (int q = threadIdx.x; q < n; q += kCellsPerBlock) dst[q] = stage[q];
+    __syncthreads();
   }
 }
 
@@ -728,7 +734,7 @@ cudaError_t launch_trace_rays(const KScene& s, int64_t n, const int64_t* src, co
 
 cudaError_t launch_build_cells(const float4* grid, int nx, int ny, int nz, CellCoef* cells,
                                cudaStream_t stream) {
-  build_cells_kernel<<<148 * 8, 256, 0, stream>>>(grid, nx, ny, nz, cells);
+  build_cells_kernel<<<148 * 6, kCellsPerBlock, 0, stream>>>(grid, nx, ny, nz, cells);
   return cudaGetLastError();
 }
 
