@@ -877,9 +877,9 @@ int rb_set_field_gvol(rb_ctx* ctx, const char* path, const double* z_center,
 
 int rb_clear_field(rb_ctx* ctx) {
   if (!ctx) return RB_E_INVALID;
-  for (Device& dev : ctx->devs) free_field(dev);
   for (Device& dev : ctx->devs) {
-    cudaSetDevice(dev.ordinal);
+    free_field(dev);
+    set_l2_window(dev);  // no field: clears the stream's access-policy window
     for (Buf& b : dev.f64) b.release();
   }
   ctx->has_field = false;
