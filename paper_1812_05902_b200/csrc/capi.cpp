@@ -429,14 +429,14 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   k.split = emitter_split(ctx, s, k);
   if (k.split > 1) {
     const size_t units = work.size() * static_cast<size_t>(k.split);
-    RB_CUDA(ctx, dev.hit_part.ensure(sizeof(double) * 2 * units));
+    RB_CUDA(ctx, dev.hit_part.ensure(sizeof(long long) * 2 * units));
     RB_CUDA(ctx, dev.landed_part.ensure(sizeof(long long) * units));
-    k.hit_part = dev.hit_part.as<double>();
+    k.hit_part = dev.hit_part.as<long long>();
     k.landed_part = dev.landed_part.as<long long>();
     if (k.pair) {
-      RB_CUDA(ctx, dev.hit_part0.ensure(sizeof(double) * 2 * units));
+      RB_CUDA(ctx, dev.hit_part0.ensure(sizeof(long long) * 2 * units));
       RB_CUDA(ctx, dev.landed_part0.ensure(sizeof(long long) * units));
-      k.hit_part0 = dev.hit_part0.as<double>();
+      k.hit_part0 = dev.hit_part0.as<long long>();
       k.landed_part0 = dev.landed_part0.as<long long>();
     }
   }

@@ -262,6 +262,14 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
   }
 }
 
+// DotHitStats::hit_sum is accumulated in fixed point, 2^-40 m per unit
+// (9.1e-13 m, 1e-7 of a 10 um pixel; a sensor-plane coordinate is < 2^36 units,
+// so 2^27 rays fit an int64): integer sums are exact, so the statistic is the
+// same for any assignment of rays to threads, chunks, CTAs or GPUs.
+constexpr double kHitScale = 1099511627776.0;  // 2^40
+__device__ __forceinline__ long long hit_fixed(double u) { return __double2ll_rn(u * kHitScale); }
+__device__ __forceinline__ double hit_double(long long s) { return (double)s * (1.0 / kHitScale); }
+
 // Deterministic block sum (fixed shuffle tree, fixed warp order).
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
@@ -299,17 +307,17 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
   // Per-thread emitter accumulators and the GRIN entry state live in shared
   // memory, not registers: they change once per ray, and keeping them out of
   // the register file during the RK4 loop is what lets K1 fit its budget.
-  __shared__ double sh_uv[2][kBlock];
+  __shared__ long long sh_uv[2][kBlock];      // hit sums, fixed point (kHitScale)
   __shared__ unsigned sh_cnt[6][kBlock];     // landed, lost, aperture, miss, tir, smiss
   __shared__ unsigned long long sh_steps[kBlock];  // RK4 steps (64-bit: rays x max_steps)
   __shared__ unsigned sh_st32[kBlock];             // the ray in flight's steps
   __shared__ double sh_rt[kBlock][7];        // R0, T0 of the ray in flight (grin.cuh)
-  __shared__ double sh_d[2][kWarps];
+  __shared__ long long sh_d[2][kWarps];
   __shared__ unsigned long long sh_l[7][kWarps];
   // bos_run pair mode (rb_trace_bos_pair): the no-field leg's accumulators
-  __shared__ double sh_uv0[2][kBlock];
+  __shared__ long long sh_uv0[2][kBlock];
   __shared__ unsigned sh_cnt0[7][kBlock];
-  __shared__ double sh_d0[2][kWarps];
+  __shared__ long long sh_d0[2][kWarps];
   __shared__ unsigned long long sh_l0[7][kWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = S.rays;
@@ -336,8 +344,8 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
       sh_box[2] = sh_box[3] = -1;
       sh_tile[0] = sh_tile[1] = sh_tile[2] = sh_tile[3] = 0;
     }
-    sh_uv[0][tid] = sh_uv[1][tid] = 0.0;
-    sh_uv0[0][tid] = sh_uv0[1][tid] = 0.0;
+    sh_uv[0][tid] = sh_uv[1][tid] = 0ll;
+    sh_uv0[0][tid] = sh_uv0[1][tid] = 0ll;
 #pragma unroll
     for (int j = 0; j < 6; ++j) sh_cnt[j][tid] = 0u;
 #pragma unroll
@@ -351,6 +359,9 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
     // One loop, one trace_ray call site: iteration 0 is the pilot, after which
     // the CTA places the tile.  __syncwarp() reconverges the lanes after every
     // ray so a warp never splits into groups running different rays' RK4 loops.
+    // (Taking the patches after the pilot from a shared counter instead, so
+    // warps with short rays take more, measured no gain: the unit-end barrier
+    // waits on the last ray's length, not on the patch count.)
     for (int k = kb; k < ke; ++k) {
       int i = -1;
       const int slot = k * kWarps + warp;
@@ -372,8 +383,8 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
             const RayResult r0 = finish_ray<kField>(S, so, d, false, sh_rt[tid], &sh_st32[tid]);
             sh_cnt0[r0.status][tid] += 1u;
             if (r0.status == 0) {
-              sh_uv0[0][tid] += r0.u;
-              sh_uv0[1][tid] += r0.v;
+              sh_uv0[0][tid] += hit_fixed(r0.u);
+              sh_uv0[1][tid] += hit_fixed(r0.v);
             }
             r = finish_ray<kField>(S, so, d, true, sh_rt[tid], &sh_st32[tid]);
           } else {
@@ -424,8 +435,8 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
       if (r.status >= 0) {
         sh_cnt[r.status][tid] += 1u;
         if (r.status == 0) {
-          sh_uv[0][tid] += r.u;
-          sh_uv[1][tid] += r.v;
+          sh_uv[0][tid] += hit_fixed(r.u);
+          sh_uv[1][tid] += hit_fixed(r.v);
           if (S.accumulate)
             deposit(S, r.u, r.v, tile, vtile[0], vtile[1], vtile[2], vtile[3],
                     (uint32_t)(mix_bits(ekey + (uint64_t)i) >> 32), wsh);
@@ -435,8 +446,8 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
     }
 
     // per-emitter stats: DotHitStats (bos.hpp:71-74) + counters, fixed order
-    double su = warp_sum(sh_uv[0][tid]);
-    double sv = warp_sum(sh_uv[1][tid]);
+    const long long su = warp_sum(sh_uv[0][tid]);
+    const long long sv = warp_sum(sh_uv[1][tid]);
     unsigned long long cnt[7];
 #pragma unroll
     for (int j = 0; j < 6; ++j) cnt[j] = warp_sum((unsigned long long)sh_cnt[j][tid]);
@@ -448,8 +459,8 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
       for (int j = 0; j < 7; ++j) sh_l[j][warp] = cnt[j];
     }
     if (kPair) {
-      const double su0 = warp_sum(sh_uv0[0][tid]);
-      const double sv0 = warp_sum(sh_uv0[1][tid]);
+      const long long su0 = warp_sum(sh_uv0[0][tid]);
+      const long long sv0 = warp_sum(sh_uv0[1][tid]);
       unsigned long long c0[7];
 #pragma unroll
       for (int j = 0; j < 7; ++j) c0[j] = warp_sum((unsigned long long)sh_cnt0[j][tid]);
@@ -472,7 +483,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
       }
     }
     if (tid == 0) {
-      double a = 0.0, b = 0.0;
+      long long a = 0, b = 0;
       unsigned long long l[7] = {0, 0, 0, 0, 0, 0, 0};
       for (int k = 0; k < kWarps; ++k) {
         a += sh_d[0][k];
@@ -481,15 +492,19 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
         for (int j = 0; j < 7; ++j) l[j] += sh_l[j][k];
       }
       const int src = sh_src;
-      double* hs = S.split > 1 ? S.hit_part + 2 * (size_t)sh_work : S.hit_sum + 2 * src;
-      hs[0] = a;
-      hs[1] = b;
+      if (S.split > 1) {
+        S.hit_part[2 * (size_t)sh_work] = a;
+        S.hit_part[2 * (size_t)sh_work + 1] = b;
+      } else {
+        S.hit_sum[2 * src] = hit_double(a);
+        S.hit_sum[2 * src + 1] = hit_double(b);
+      }
       *(S.split > 1 ? S.landed_part + sh_work : S.landed + src) = (long long)l[0];
 #pragma unroll
       for (int j = 1; j < 7; ++j)
         if (l[j]) atomicAdd(&S.counters[j - 1], l[j]);
       if (kPair) {
-        double a0 = 0.0, b0 = 0.0;
+        long long a0 = 0, b0 = 0;
         unsigned long long m[7] = {0, 0, 0, 0, 0, 0, 0};
         for (int k = 0; k < kWarps; ++k) {
           a0 += sh_d0[0][k];
@@ -497,9 +512,13 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
 #pragma unroll
           for (int j = 0; j < 7; ++j) m[j] += sh_l0[j][k];
         }
-        double* hs0 = S.split > 1 ? S.hit_part0 + 2 * (size_t)sh_work : S.hit_sum0 + 2 * src;
-        hs0[0] = a0;
-        hs0[1] = b0;
+        if (S.split > 1) {
+          S.hit_part0[2 * (size_t)sh_work] = a0;
+          S.hit_part0[2 * (size_t)sh_work + 1] = b0;
+        } else {
+          S.hit_sum0[2 * src] = hit_double(a0);
+          S.hit_sum0[2 * src + 1] = hit_double(b0);
+        }
         *(S.split > 1 ? S.landed_part0 + sh_work : S.landed0 + src) = (long long)m[0];
 #pragma unroll
         for (int j = 1; j < 6; ++j)
@@ -514,7 +533,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
 __global__ void emitter_stats_kernel(const __grid_constant__ KScene S) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < S.n_work; e += gridDim.x * blockDim.x) {
     const int src = S.order[e];
-    double a = 0.0, b = 0.0;
+    long long a = 0, b = 0;
     long long l = 0;
     for (int c = 0; c < S.split; ++c) {
       const size_t w = (size_t)e * S.split + c;
@@ -522,11 +541,11 @@ __global__ void emitter_stats_kernel(const __grid_constant__ KScene S) {
       b += S.hit_part[2 * w + 1];
       l += S.landed_part[w];
     }
-    S.hit_sum[2 * src] = a;
-    S.hit_sum[2 * src + 1] = b;
+    S.hit_sum[2 * src] = hit_double(a);
+    S.hit_sum[2 * src + 1] = hit_double(b);
     S.landed[src] = l;
     if (S.pair) {
-      double a0 = 0.0, b0 = 0.0;
+      long long a0 = 0, b0 = 0;
       long long l0 = 0;
       for (int c = 0; c < S.split; ++c) {
         const size_t w = (size_t)e * S.split + c;
@@ -534,8 +553,8 @@ __global__ void emitter_stats_kernel(const __grid_constant__ KScene S) {
         b0 += S.hit_part0[2 * w + 1];
         l0 += S.landed_part0[w];
       }
-      S.hit_sum0[2 * src] = a0;
-      S.hit_sum0[2 * src + 1] = b0;
+      S.hit_sum0[2 * src] = hit_double(a0);
+      S.hit_sum0[2 * src + 1] = hit_double(b0);
       S.landed0[src] = l0;
     }
   }

@@ -127,9 +127,9 @@ struct KScene {
   // to part[work * split + chunk] and emitter_stats_kernel sums them in chunk
   // order (deterministic).  split == 1 writes hit_sum / landed directly.
   int32_t split, pad_split;
-  double* hit_part;                 // 2 * n_work * split (and *_part0 in pair mode)
+  long long* hit_part;              // 2 * n_work * split, fixed point (kernels.cu kHitScale)
   long long* landed_part;
-  double* hit_part0;
+  long long* hit_part0;
   long long* landed_part0;
 };
 
