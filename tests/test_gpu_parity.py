@@ -196,3 +196,27 @@ def test_wide_and_degenerate_spots_match_oracle(tracer, oracle, dtau_scale, wind
     assert rel_l2(a.image, b.image) < IMG_RTOL
     # energy: the dithered fixed point is unbiased; its noise stays ~1e-6
     assert abs(a.image.sum() - b.image.sum()) / b.image.sum() < 2e-6
+
+
+@pytest.mark.parametrize("n_rays", [1, 2, 7, 300, 1000, 1500, 5000])
+@pytest.mark.parametrize("sampling", [0, 1])
+def test_lattice_sizes_match_oracle(tracer, oracle, n_rays, sampling):
+    """Bundle sizes whose stratified lattice is not square or not a multiple of
+    the 8x4 warp patch (partial / empty top rows, n == 1), in
+    both sampling modes, through the field: the band-ordered patch mapping must
+    visit every ray exactly once."""
+    scene, field, g = load("blob")
+    scene.rays_per_source = n_rays
+    scene.sampling = sampling
+    tracer.set_field(field)
+    a = tracer.run_trace(scene, True, True)
+    b = oracle.trace(scene, field, True, True)
+    assert a.report["emitted"] == b.report["emitted"] == scene.n_sources * n_rays
+    for k in ("landed", "lost", "blocked_aperture", "blocked_miss", "blocked_tir",
+              "blocked_sensor_miss"):
+        assert a.report[k] == b.report[k], k
+    assert np.array_equal(a.landed, b.landed)
+    m = a.landed > 0
+    d = np.abs(a.hit_sum[m] / a.landed[m, None] - b.hit_sum[m] / b.landed[m, None]).max(initial=0)
+    assert d / scene.sensor.pitch < PX_TOL
+    assert rel_l2(a.image, b.image) < IMG_RTOL
