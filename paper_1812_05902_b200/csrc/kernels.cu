@@ -1,15 +1,19 @@
 // kernels.cu — the B200 render pipeline (sm_100a).
 //
 // K1 render_emitters fuses the four stages of process_source
-// (reference proj/src/engine.cpp:107-140) for one emitter per CTA:
+// (reference proj/src/engine.cpp:107-140) for one chunk of one emitter per CTA
+// (an emitter is split over KScene::split CTAs):
 //   stage 1  ray generation        raygen.cpp:12-88   FP64, counter RNG (core.hpp:80-107)
-//   stage 2  GRIN RK4 propagation   grin.cpp:23-134    FP32 perturbation form over a float4 grid
+//   stage 2  GRIN RK4 propagation   grin.cpp:23-134    FP32 perturbation form; the cell
+//            under the ray cached in registers as a polynomial (per-cell table or the
+//            float4 nodes), evaluated with packed FFMA2
 //   stage 3  optics chain           optics.cpp:15-158  FP64 in registers
 //   stage 4  sensor + deposition    sensor.cpp:27-122  FP64 hit, FP32 erf spot weights,
-//            u32 shared-memory tile (native ATOMS.ADD) flushed with u64 global reductions
+//            u32 shared-memory tile (branch-free RED rows) flushed with u64 global reductions
 // plus make_tile/composite_tile (engine.cpp:142-187): the image is a 64-bit
-// fixed-point sum (radiance * 2^31), so it is order-independent and bit-identical
-// for any emitter order, CTA count or GPU count.
+// fixed-point sum (radiance * 2^31) and the DotHitStats sums are fixed point too,
+// so every output is order-independent and bit-identical for any emitter order,
+// chunking, CTA count or GPU count.
 #include "kernels.h"
 
 #include <math.h>
