@@ -132,3 +132,27 @@ def test_kernel_launch_count_is_reported(tracer, monkeypatch):
     assert tracer.run_trace(scene, True, False).report["kernel_launches"] == 1
     monkeypatch.setenv("RAYBOS_SPLIT", "4")
     assert tracer.run_trace(scene, True, True).report["kernel_launches"] == 3
+
+
+def test_large_grid_cell_table_matches_nodes(tracer, monkeypatch):
+    """Config 5's 1024^3 grid (17 GB of nodes + a 137 GB cell table on one
+    B200): 32-bit cell / node indexing and the table build at full size give
+    the node path's bits on sampled rays, through real deflections."""
+    from paper_1812_05902_b200 import scenes
+    scene, grid, info, desc = scenes.build("large", scale=0.002)
+    rng = np.random.default_rng(3)
+    src = rng.integers(0, scene.n_sources, 2048)
+    ray = rng.integers(0, scene.rays_per_source, 2048).astype(np.int32)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RAYBOS_CELL_TABLE", flag)
+        tracer.set_field(grid)
+        out[flag] = (tracer.field_bytes(), tracer.trace_rays(scene, src, ray, True))
+    (b1, (uv1, st1, n1)), (b0, (uv0, st0, n0)) = out["1"], out["0"]
+    tracer.set_field(None)
+    assert b1 > 100e9 and b0 == 1024 ** 3 * 16
+    assert np.array_equal(st1, st0) and np.array_equal(n1, n0)
+    assert np.array_equal(uv1, uv0, equal_nan=True)
+    free, _ = tracer.trace_rays(scene, src, ray, False)[:2]
+    ok = st1 == 0
+    assert np.abs(uv1[ok] - free[ok]).max() / scene.sensor.pitch > 0.1  # the medium deflects
