@@ -182,9 +182,12 @@ def cpu_baseline_entry(scene, grid, target_s: float):
     run, m, kind, thr = cpu_reference(scene, grid, target_s)
     t, thr = run(m)
     rays = m * scene.rays_per_source
+    # the measured sample rate and its linear extrapolation to
+    # the whole image (emitters are drawn at random, so the sample is unbiased)
     return {"value": rays / t, "unit": "rays/s", "cores": thr, "kind": kind,
             "sample": f"{m} of {scene.n_sources} emitters x {scene.rays_per_source} rays "
-                      f"({rays:.3g} rays, {t:.1f} s), same grid/optics/sensor, image accumulated"}
+                      f"({rays:.3g} rays, {t:.1f} s), same grid/optics/sensor, image accumulated",
+            "extrapolated_s_per_image": scene.n_sources * scene.rays_per_source / (rays / t)}
 
 
 # ------------------------------------------------------------------- main
