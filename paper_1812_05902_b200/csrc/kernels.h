@@ -153,6 +153,13 @@ cudaError_t launch_build_fp64(const float* rho, int nx, int ny, int nz, double k
                               double* n, double* gx, double* gy, double* gz, cudaStream_t stream);
 cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream);
 cudaError_t launch_emitter_stats(const KScene& s, cudaStream_t stream);
+// the no-medium instantiations, compiled in their own translation unit
+// (kernels_nomedium.cu); launch_render / launch_trace_rays dispatch to them
+int render_occupancy_nomedium(int blocks_per_sm[2]);
+cudaError_t launch_render_nomedium(const KScene& s, int grid, cudaStream_t stream);
+cudaError_t launch_trace_rays_nomedium(const KScene& s, int64_t n, const int64_t* src,
+                                       const int32_t* ray, double* uv, int32_t* status,
+                                       int32_t* steps, cudaStream_t stream);
 // resident CTAs per SM of each render_emitters instantiation, [pair][field mode]
 int render_occupancy(int blocks_per_sm[2][3]);
 int field_mode(const KScene& s);  // 0 no medium, 1 nodes, 2 cell table

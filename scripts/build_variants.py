@@ -3,7 +3,7 @@
 usage: EXTRA="-DRB_MINB_CELLS=2 ..." TAG=_x python scripts/build_variants.py
 Recompiles kernels.cu with the extra defines (RB_BLOCK, RB_MINB, RB_MINB_CELLS,
 RB_MINB_NOFIELD, RB_UNIFORM_RELOAD, RB_DITHER, RB_STEP_UNROLL, RB_MAX_SPOT ...)
-and links it with the current capi / FP64 objects of paper_1812_05902_b200/_build
+and links it with the other current objects of paper_1812_05902_b200/_build
 into paper_1812_05902_b200/_variants/libraybos_gpu<TAG>.so."""
 import os
 import subprocess
@@ -21,7 +21,7 @@ subprocess.run([NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", *
                 *os.environ.get("EXTRA", "").split(), f"-I{ROOT}/include", "-c",
                 os.path.join(PKG, "csrc", "kernels.cu"), "-o", obj], check=True)
 lib = os.path.join(OUT, f"libraybos_gpu{tag}.so")
-subprocess.run([NVCC, "-shared", *ARCH, os.path.join(PKG, "_build", "capi.cpp.o"),
-                os.path.join(PKG, "_build", "kernels_fp64.cu.o"), obj, "-o", lib, "-ldl", "-lpthread"],
-               check=True)
+others = [os.path.join(PKG, "_build", f) for f in sorted(os.listdir(os.path.join(PKG, "_build")))
+          if f.endswith(".o") and f != "kernels.cu.o"]
+subprocess.run([NVCC, "-shared", *ARCH, *others, obj, "-o", lib, "-ldl", "-lpthread"], check=True)
 print(lib)

@@ -3,7 +3,8 @@ render_emitters instantiation (dev aid).  usage: loop_sass.py lib.so ILb0ELi2E""
 import re, subprocess, sys
 sass = subprocess.run(["cuobjdump", "-sass", sys.argv[1]], capture_output=True, text=True).stdout
 fn = sys.argv[2]
-body = sass[sass.index("Function : _ZN3rbk15render_emitters" + fn):]
+m = re.search(r"Function : \S*render_emitters" + fn, sass)
+body = sass[m.start():]
 body = body[:body.index("Function :", 20)] if "Function :" in body[20:] else body
 lines = [l for l in body.splitlines() if re.match(r'\s+/\*[0-9a-f]{4,5}\*/', l)]
 addr = [int(re.match(r'\s+/\*([0-9a-f]+)\*/', l).group(1), 16) for l in lines]

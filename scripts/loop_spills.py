@@ -1,7 +1,8 @@
 """Reports spill instructions inside K1's GRIN loop for a cubin/.so (dev aid)."""
 import re, subprocess, sys
 sass = subprocess.run(["cuobjdump", "-sass", sys.argv[1]], capture_output=True, text=True).stdout
-body = sass[sass.index("Function : _ZN3rbk15render_emitters"):]
+m = re.search(r"Function : \S*render_emitters", sass)
+body = sass[m.start():]
 body = body[:body.index("Function :", 20)] if "Function :" in body[20:] else body
 lines = [l for l in body.splitlines() if re.match(r'\s+/\*[0-9a-f]{4,5}\*/', l)]
 addr = [int(re.match(r'\s+/\*([0-9a-f]+)\*/', l).group(1), 16) for l in lines]
