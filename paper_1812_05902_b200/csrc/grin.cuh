@@ -13,7 +13,7 @@
 // The unperturbed line R0 + T0 * xi is never accumulated (it is re-evaluated
 // from the step index), so FP32 rounding cannot drift the ray; R0, T0 and the
 // exit cut-back are FP64 (<= 4e-5 px vs FP64).
-// Included by kernels.cu inside namespace rbk::(anonymous), after the FP64
+// Included by render.cuh inside namespace rbk::(anonymous), after the FP64
 // vector helpers and the status enums.
 #pragma once
 

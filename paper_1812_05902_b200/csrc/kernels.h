@@ -127,7 +127,7 @@ struct KScene {
   // to part[work * split + chunk] and emitter_stats_kernel sums them in chunk
   // order (deterministic).  split == 1 writes hit_sum / landed directly.
   int32_t split, pad_split;
-  long long* hit_part;              // 2 * n_work * split, fixed point (kernels.cu kHitScale)
+  long long* hit_part;              // 2 * n_work * split, fixed point (render.cuh kHitScale)
   long long* landed_part;
   long long* hit_part0;
   long long* landed_part0;

@@ -1,4 +1,4 @@
-// stages.cuh — FP64 stages of the per-ray pipeline shared by K1 (kernels.cu,
+// stages.cuh — FP64 stages of the per-ray pipeline shared by K1 (render.cuh,
 // compiled with FMA contraction) and the FP64 validation kernels
 // (kernels_fp64.cu, compiled with -fmad=false so every operation rounds like
 // the reference's x86-64 build).  Included inside namespace rbk::(anonymous).
