@@ -5,6 +5,7 @@
 // stages.cuh) without perturbing the register allocation of the RK4 loop the
 // field instantiations in kernels.cu carry.
 #define RB_FAST_DIV 1
+#define RB_COMPACT_SLOW_ROWS 1
 #include "kernels.h"
 #include "render.cuh"
 

@@ -223,6 +223,19 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
         }
       } else {
         float wr[kMaxSpot];
+#if RB_COMPACT_SLOW_ROWS
+        // rolled: rows off the tile are rare, and a smaller kernel misses the
+        // instruction cache less (the no-medium kernel's main stall)
+#pragma unroll 1
+        for (int k = 0; k < ncol; ++k) {
+          const int c = c0 + k;
+          if (c >= 0 && c < S.W) {
+            const float wk = reinterpret_cast<const float*>(wsh + (k >> 2) * kBlock)[k & 3];
+            const uint32_t f = dround(wk * row_w, w);
+            if (f) add_px(S, tile, tc0, tr0, tw, th, c, r, f);
+          }
+        }
+#else
         lds_weights(wsh, wr, 3);
 #pragma unroll
         for (int k = 0; k < kMaxSpot; ++k) {
@@ -232,6 +245,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
             if (f) add_px(S, tile, tc0, tr0, tw, th, c, r, f);
           }
         }
+#endif
       }
     }
   } else {  // wide spots: recompute column weights per pixel
