@@ -222,10 +222,10 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
           red_row<kMaxSpot>(trow, wr, row_w, w);
         }
       } else {
-        float wr[kMaxSpot];
 #if RB_COMPACT_SLOW_ROWS
         // rolled: rows off the tile are rare, and a smaller kernel misses the
-        // instruction cache less (the no-medium kernel's main stall)
+        // instruction cache less (the no-medium kernel's main stall; the field
+        // kernels measured 1% slower rolled, so they keep the unrolled row)
 #pragma unroll 1
         for (int k = 0; k < ncol; ++k) {
           const int c = c0 + k;
@@ -236,6 +236,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
           }
         }
 #else
+        float wr[kMaxSpot];
         lds_weights(wsh, wr, 3);
 #pragma unroll
         for (int k = 0; k < kMaxSpot; ++k) {
