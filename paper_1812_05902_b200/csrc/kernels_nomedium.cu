@@ -6,6 +6,7 @@
 // field instantiations in kernels.cu carry.
 #define RB_FAST_DIV 1
 #define RB_COMPACT_SLOW_ROWS 1
+#define RB_COMPACT_OPTICS 1
 #include "kernels.h"
 #include "render.cuh"
 

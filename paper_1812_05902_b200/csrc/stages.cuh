@@ -172,6 +172,19 @@ __device__ __forceinline__ int optics_chain(const KScene& S, double3& o, double3
       o = hp;
       d = normalized((focal_point - hp) * (el.focal > 0.0 ? 1.0 : -1.0));
     } else if (el.kind == 1) {  // propagate_through_lens, optics.cpp:85-106
+#if RB_COMPACT_OPTICS
+      // the two surfaces as one rolled loop: the same operations, half the code
+      // (RB_COMPACT_OPTICS: the instruction-cache-bound no-medium kernel)
+#pragma unroll 1
+      for (int sf = 0; sf < 2; ++sf) {
+        const DSurface& srf = sf ? el.back : el.front;
+        double3 hp, hn, out_dir;
+        if (!sphere_hit(o, d, srf, hp, hn)) return kBrMissed;
+        if (!refract(d, hn, srf.n_before, srf.n_after, out_dir)) return kBrTir;
+        o = hp;
+        d = out_dir;
+      }
+#else
       double3 hp, hn, in_dir, out_dir;
       if (!sphere_hit(o, d, el.front, hp, hn)) return kBrMissed;
       if (!refract(d, hn, el.front.n_before, el.front.n_after, in_dir)) return kBrTir;
@@ -180,6 +193,7 @@ __device__ __forceinline__ int optics_chain(const KScene& S, double3& o, double3
       if (!refract(in_dir, bn, el.back.n_before, el.back.n_after, out_dir)) return kBrTir;
       o = bp;
       d = out_dir;
+#endif
     } else {  // reflect_on_mirror, optics.cpp:134-141
       double3 hp, hn;
       if (!sphere_hit(o, d, el.front, hp, hn)) return kBrMissed;
