@@ -3,6 +3,6 @@ for sc in "optics 1" "piv 1"; do
   set -- $sc
   CMD="python scripts/run_scene.py $1 $2"
   $CMD > gpurun_out/plain_$1.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:render_emitters -s 1 -c 1 -o gpurun_out/prof9_$1 $CMD > gpurun_out/ncu9_$1.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:render_emitters -s 1 -c 1 -o gpurun_out/prof10_$1 $CMD > gpurun_out/ncu10_$1.log 2>&1
   echo "$1 rc=$?"; cat gpurun_out/plain_$1.log
 done
