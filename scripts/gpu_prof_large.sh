@@ -1,5 +1,4 @@
 cd "${GRAFT_REPO_ROOT:-.}"
-export RAYBOS_CELL_TABLE=2
 CMD="python scripts/run_scene.py large 0.003"
 $CMD > gpurun_out/plain_large.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:render_emitters -s 1 -c 1 -o gpurun_out/prof_large $CMD > gpurun_out/ncu_large.log 2>&1
