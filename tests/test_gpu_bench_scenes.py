@@ -81,3 +81,34 @@ def test_bench_scene_image_matches_oracle(tracer, oracle, bench_scene):
     d = np.abs(a.hit_sum[m] / a.landed[m, None] - b.hit_sum[m] / b.landed[m, None]).max()
     assert d / scene.sensor.pitch < PX_TOL, (name, d)
     assert rel_l2(a.image, b.image) < IMG_RTOL, (name, rel_l2(a.image, b.image))
+
+
+@pytest.mark.parametrize("name", ["tomo", "bos", "optics"])
+def test_energy_is_conserved_at_bench_resolution(tracer, name):
+    """Size-independent property (test_sensor.cpp's energy check, at bench
+    scale): every landed ray deposits radiance 1/N over its spot window, so for
+    emitters whose spots lie well inside the frame the fixed-point image sums to
+    landed / N up to the dithered rounding (< 1e-6 relative)."""
+    from paper_1812_05902_b200 import scenes
+    scene, grid, info, desc = scenes.build(name, scale=0.005 if name != "bos" else 0.02)
+    tracer.set_field(grid)
+    n = scene.n_sources
+    src = np.repeat(np.arange(n), 64)
+    ray = np.tile(np.linspace(0, scene.rays_per_source - 1, 64).astype(np.int32), n)
+    uv, st, _ = tracer.trace_rays(scene, src, ray, grid is not None)
+    p = scene.sensor.pitch
+    col = uv[:, 0] / p + 0.5 * scene.width
+    row = 0.5 * scene.height - uv[:, 1] / p
+    margin = 40.0
+    inside = (st != 0) | ((col > margin) & (col < scene.width - margin) &
+                          (row > margin) & (row < scene.height - margin))
+    keep = np.flatnonzero(inside.reshape(n, 64).all(axis=1) &
+                          (st.reshape(n, 64) == 0).any(axis=1))[:24]
+    assert keep.size >= 4, "too few emitters fully in frame"
+    if scene.source_ids is None:
+        scene.source_ids = np.arange(n, dtype=np.int64)
+    scene.sources = scene.sources[keep].copy()
+    scene.source_ids = scene.source_ids[keep].copy()
+    res = tracer.run_trace(scene, grid is not None, True)
+    expected = res.landed.sum() / scene.rays_per_source
+    assert abs(res.image.sum() - expected) / expected < 1e-6
