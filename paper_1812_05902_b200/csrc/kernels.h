@@ -25,7 +25,10 @@ constexpr int kMinBlocksNoField = RB_MINB_NOFIELD;  // the same for scenes witho
 #define RB_MINB_CELLS 3  // cell-table GRIN loop fits 80 registers: bos +3.5%, 1024^3 +5% (not pair mode)
 #endif
 constexpr int kMinBlocksCells = RB_MINB_CELLS;  // ... and for fields read from the cell table
-constexpr int kTileCap = 6144;       // u32 entries of the per-emitter shared tile (24 KB)
+#ifndef RB_TILE_CAP
+#define RB_TILE_CAP 6144
+#endif
+constexpr int kTileCap = RB_TILE_CAP;  // u32 entries of the per-emitter shared tile (24 KB)
 #ifndef RB_MAX_SPOT
 #define RB_MAX_SPOT 12  // 16 measured 10-40% slower (code size); bench spots are <= 11 wide
 #endif
