@@ -220,3 +220,50 @@ def test_lattice_sizes_match_oracle(tracer, oracle, n_rays, sampling):
     d = np.abs(a.hit_sum[m] / a.landed[m, None] - b.hit_sum[m] / b.landed[m, None]).max(initial=0)
     assert d / scene.sensor.pitch < PX_TOL
     assert rel_l2(a.image, b.image) < IMG_RTOL
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_randomised_scenes_match_oracle(tracer, oracle, seed):
+    """Fuzz around the fixtures: random emitter positions (inside and around the
+    field of view), bundle sizes, sampling mode, RNG seed, field strength (the
+    fixture's index excess and gradients scaled together, up to 6x) and step
+    size, each checked live against the oracle."""
+    from paper_1812_05902_b200.scene import FieldNodes
+    rng = np.random.default_rng(1000 + seed)
+    name = ["blob", "field3d", "shock_particles"][seed % 3]
+    scene, field, g = load(name)
+    lo, hi = scene.sources.min(0), scene.sources.max(0)
+    span = np.maximum(hi - lo, 1e-3)
+    n_src = int(rng.integers(4, 24))
+    scene.sources = lo - 0.2 * span + rng.random((n_src, 3)) * 1.4 * span
+    if name != "shock_particles":
+        scene.sources[:, 2] = lo[2]  # dots / particles on their plane
+    scene.source_ids = None
+    scene.rays_per_source = int(rng.integers(1, 2500))
+    scene.sampling = int(rng.integers(0, 2))
+    scene.seed = int(rng.integers(0, 2**31))
+    scene.delta_xi *= float(rng.uniform(0.6, 1.5))
+    a = float(rng.uniform(0.2, 6.0))
+    f = FieldNodes(field.nx, field.ny, field.nz, field.origin, field.spacing,
+                   1.0 + a * (field.n - 1.0), a * field.gx, a * field.gy, a * field.gz)
+    tracer.set_field(f)
+    r = tracer.run_trace(scene, True, True)
+    o = oracle.trace(scene, f, True, True)
+    for k in ("emitted", "landed", "lost", "blocked_aperture", "blocked_miss", "blocked_tir",
+              "blocked_sensor_miss"):
+        assert r.report[k] == o.report[k], (k, r.report[k], o.report[k])
+    assert np.array_equal(r.landed, o.landed)
+    m = r.landed > 0
+    if m.any():
+        d = np.abs(r.hit_sum[m] / r.landed[m, None] - o.hit_sum[m] / o.landed[m, None]).max()
+        assert d / scene.sensor.pitch < PX_TOL
+    if o.image.any():
+        assert rel_l2(r.image, o.image) < IMG_RTOL
+    src = rng.integers(0, n_src, 256)
+    ray = rng.integers(0, scene.rays_per_source, 256).astype(np.int32)
+    uv, st, steps = tracer.trace_rays(scene, src, ray, True)
+    ruv, rst, rsteps, _ = oracle.trace_rays(scene, f, src, ray, True)
+    assert np.array_equal(st, rst)
+    ok = st == 0
+    assert np.abs(uv[ok] - ruv[ok]).max(initial=0.0) / scene.sensor.pitch < PX_TOL
+    assert np.abs(steps - rsteps).max(initial=0) <= 1
