@@ -58,7 +58,8 @@ def test_ctypes_layout_matches_c(tmp_path):
         "rb_field_desc": ["nx", "ny", "nz", "origin", "spacing"],
         "rb_trace_out": ["hit_sum", "landed", "image", "emitted", "landed_total", "lost",
                          "blocked_aperture", "blocked_miss", "blocked_tir", "blocked_sensor_miss",
-                         "wall_seconds", "threads", "config_hash", "total_steps", "kernel_ms"],
+                         "wall_seconds", "threads", "config_hash", "total_steps", "kernel_ms",
+                         "quantized", "gain", "bit_depth", "kernel_launches"],
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "raybos_gpu.h"', 'int main(void){']
     for st, fs in fields.items():
