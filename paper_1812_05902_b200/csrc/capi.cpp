@@ -340,20 +340,29 @@ struct PartialOut {
 // L2; each chunk costs one pilot and one tile flush.  The chunk is sized to
 // about 4e5 RK4 steps, estimating the steps per ray as the box depth along the
 // pupil axis over h (measured optimum: tomo 4-8, bos 16, 1024^3 32; bos +18%,
-// 1024^3 +4%, tomo +1% over one CTA per emitter).  No field: one CTA per
-// emitter.  RAYBOS_SPLIT overrides.
-int emitter_split(const rb_ctx* ctx, const rb_scene* s, const rbk::KScene& k) {
-  if (const char* e = std::getenv("RAYBOS_SPLIT")) return std::max(1, std::min(64, std::atoi(e)));
-  if (!k.with_field || !(k.h > 0.0)) return 1;
-  const double ext[3] = {ctx->box_hi.x - ctx->box_lo.x, ctx->box_hi.y - ctx->box_lo.y,
-                         ctx->box_hi.z - ctx->box_lo.z};
-  const double ax[3] = {s->pupil_axis.x, s->pupil_axis.y, s->pupil_axis.z};
-  const double an = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
-  double depth = 0.0;
-  for (int a = 0; a < 3; ++a) depth += std::fabs(ext[a] * ax[a]) / (an > 0.0 ? an : 1.0);
-  const double steps = std::min<double>(depth / k.h, s->max_steps);
-  const double split = std::round(static_cast<double>(s->rays_per_source) * steps / 4e5);
-  return static_cast<int>(std::max(1.0, std::min(64.0, split)));
+// 1024^3 +4%, tomo +1% over one CTA per emitter).  Independently, a work list
+// shorter than the resident CTAs is split until every CTA gets two units (3
+// emitters x 4e6 rays: 1.29 s -> 17 ms), never below one patch iteration per
+// unit.  RAYBOS_SPLIT overrides.
+int emitter_split(const rb_ctx* ctx, const rb_scene* s, const rbk::KScene& k, size_t n_work,
+                  int resident_ctas) {
+  const int iters = std::max(1, (k.patch_count + rbk::kBlock / 32 - 1) / (rbk::kBlock / 32));
+  const int cap = std::min(iters, 4096);
+  if (const char* e = std::getenv("RAYBOS_SPLIT")) return std::max(1, std::min(cap, std::atoi(e)));
+  double split = 1.0;
+  if (k.with_field && k.h > 0.0) {
+    const double ext[3] = {ctx->box_hi.x - ctx->box_lo.x, ctx->box_hi.y - ctx->box_lo.y,
+                           ctx->box_hi.z - ctx->box_lo.z};
+    const double ax[3] = {s->pupil_axis.x, s->pupil_axis.y, s->pupil_axis.z};
+    const double an = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+    double depth = 0.0;
+    for (int a = 0; a < 3; ++a) depth += std::fabs(ext[a] * ax[a]) / (an > 0.0 ? an : 1.0);
+    const double steps = std::min<double>(depth / k.h, s->max_steps);
+    split = std::min(64.0, std::round(static_cast<double>(s->rays_per_source) * steps / 4e5));
+  }
+  if (n_work > 0 && n_work < static_cast<size_t>(resident_ctas))
+    split = std::max(split, std::ceil(2.0 * resident_ctas / static_cast<double>(n_work)));
+  return static_cast<int>(std::max(1.0, std::min(static_cast<double>(cap), split)));
 }
 
 // One device renders the given work list into dev.image (already zeroed or
@@ -426,7 +435,8 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
     }
   }
   if (k.with_field && !dev.grid) return fail(ctx, RB_E_RUNTIME, "rb_trace: field not uploaded");
-  k.split = emitter_split(ctx, s, k);
+  k.split = emitter_split(ctx, s, k, work.size(),
+                          dev.sms * dev.blocks_per_sm[k.pair ? 1 : 0][rbk::field_mode(k)]);
   if (k.split > 1) {
     const size_t units = work.size() * static_cast<size_t>(k.split);
     RB_CUDA(ctx, dev.hit_part.ensure(sizeof(long long) * 2 * units));
