@@ -267,3 +267,23 @@ def test_randomised_scenes_match_oracle(tracer, oracle, seed):
     ok = st == 0
     assert np.abs(uv[ok] - ruv[ok]).max(initial=0.0) / scene.sensor.pitch < PX_TOL
     assert np.abs(steps - rsteps).max(initial=0) <= 1
+
+
+def test_few_emitters_with_big_bundles_match_oracle(tracer, oracle, monkeypatch):
+    """Fewer emitters than resident CTAs: capi.cpp emitter_split spreads each
+    bundle over hundreds of CTAs; the result must equal the oracle and, bit for
+    bit, a single-CTA-per-emitter render."""
+    scene, field, g = load("blob")
+    scene.sources = scene.sources[:2].copy()
+    scene.rays_per_source = 200_000
+    tracer.set_field(field)
+    a = tracer.run_trace(scene, True, True)
+    monkeypatch.setenv("RAYBOS_SPLIT", "1")
+    b = tracer.run_trace(scene, True, True)
+    assert np.array_equal(a.image, b.image) and np.array_equal(a.hit_sum, b.hit_sum)
+    o = oracle.trace(scene, field, True, True)
+    assert np.array_equal(a.landed, o.landed)
+    m = a.landed > 0
+    d = np.abs(a.hit_sum[m] / a.landed[m, None] - o.hit_sum[m] / o.landed[m, None]).max()
+    assert d / scene.sensor.pitch < PX_TOL
+    assert rel_l2(a.image, o.image) < IMG_RTOL
