@@ -271,11 +271,13 @@ int rb_trace_rays_fp64(rb_ctx* ctx, const rb_scene* scene, int with_field, int64
 int rb_trace_stats_fp64(rb_ctx* ctx, const rb_scene* scene, int with_field, rb_trace_out* out);
 
 /* bos_run's two traces (engine.cpp:539-540: run_trace without, then with the
- * field, identical seeds) fused into one pass: every ray is generated once and
- * followed both straight (reference leg) and through the density grid
- * (gradient leg).  Per-dot DotHitStats and counters for both legs, no images
- * (bos_run only needs images when write_images is set; use rb_trace for those).
- * Bit-identical to two rb_trace(accumulate_image = 0) calls. */
+ * field, identical seeds) in one call: on the node grid every ray is generated
+ * once and followed both straight (reference leg) and through the density grid
+ * (gradient leg); with the per-cell table the two legs run as two passes (the
+ * field kernel's occupancy makes that faster).  Per-dot DotHitStats and
+ * counters for both legs, no images (bos_run only needs images when
+ * write_images is set; use rb_trace for those).  Bit-identical to two
+ * rb_trace(accumulate_image = 0) calls. */
 int rb_trace_bos_pair(rb_ctx* ctx, const rb_scene* scene, rb_trace_out* out_reference,
                       rb_trace_out* out_gradient);
 
