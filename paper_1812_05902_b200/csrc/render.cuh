@@ -287,12 +287,13 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 // ------------------------------------------------ K1: render_emitters
-// One CTA renders one emitter at a time (persistent CTAs pull emitters from a
-// queue, so the work split never affects results).  Thread t owns the K
-// consecutive rays [t*K, t*K+K) of the bundle; its first ray is traced as a
-// pilot before any deposit so the CTA can place the emitter's shared-memory
-// tile over the pilot spots' bounding box (the pilot rays are spread over the
-// whole pupil lattice).  Deposits outside the tile go straight to global.
+// Persistent CTAs pull work units from a queue: a unit is one chunk (KScene::
+// split) of one emitter's bundle, i.e. a range of patch iterations, each of
+// which gives every warp one compact 8x4 patch of the pupil lattice (KScene::
+// band_rays).  The unit's first iteration is the pilot: its spots' bounding box
+// places the unit's shared-memory tile before any deposit; deposits outside
+// the tile go straight to global.  Every accumulator is an integer, so the
+// queue order, the split and the CTA count never change a result bit.
 // kPair: bos_run pair mode (rb_trace_bos_pair), a separate instantiation so the
 // default kernel carries none of its code or registers.
 // kField: see finish_ray (a scene without a medium gets a kernel without the
