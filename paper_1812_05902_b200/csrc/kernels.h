@@ -15,7 +15,7 @@ constexpr int kMaxElements = 8;
 #ifndef RB_MINB
 #define RB_MINB 2
 #endif
-constexpr int kBlock = RB_BLOCK;     // threads per CTA (one emitter at a time)
+constexpr int kBlock = RB_BLOCK;     // threads per CTA (one emitter chunk at a time)
 constexpr int kMinBlocks = RB_MINB;  // resident CTAs per SM the register budget targets
 #ifndef RB_MINB_NOFIELD
 #define RB_MINB_NOFIELD 4  // measured: 2 -> 4 CTAs/SM is +24% optics, +15% piv
