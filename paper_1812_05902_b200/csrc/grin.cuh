@@ -166,8 +166,11 @@ template <bool kCells>
 __device__ __forceinline__ float3 sample_d_poly(const GridView& G, CellPoly& P, float qx, float qy,
                                                 float qz) {
   float fx = qx - P.ox, fy = qy - P.oy, fz = qz - P.oz;
-  // fast path: inside the cached cell (NaN fails and takes the full path)
-  const bool stay = fminf(fminf(fx, fy), fz) >= 0.0f && fmaxf(fmaxf(fx, fy), fz) <= 1.0f;
+  // fast path: inside the cached cell.  For IEEE floats "0 <= f <= 1" is
+  // "bits(f) <= bits(1.0f)" as unsigned integers (negative values, -0.0 and
+  // NaN all compare above), so one VIMNMX3 + one ISETP test all three axes.
+  const bool stay = __vimax3_u32(__float_as_uint(fx), __float_as_uint(fy), __float_as_uint(fz)) <=
+                    0x3f800000u;
 #if RB_UNIFORM_RELOAD
   // Warp-uniform variant: when any active lane leaves its cell all active lanes
   // take the reload path.  Measured equal to the per-lane branch (the 32 rays
