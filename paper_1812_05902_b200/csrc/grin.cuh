@@ -301,7 +301,10 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
     const float qx = pcx + ndrx, qy = pcy + ndry, qz = pcz + ndrz;
     // Inside the box (grid coordinates) -> accept (grin.cpp:101-106).  NaN
     // compares false, so a non-finite state always takes the exit path.
-    if (qx >= 0.0f && qx <= G.S.g_mx && qy >= 0.0f && qy <= G.S.g_my && qz >= 0.0f && qz <= G.S.g_mz) {
+    // (as in sample_d_poly: 0 <= q <= m is bits(q) <= bits(m) unsigned)
+    if (__float_as_uint(qx) <= __float_as_uint(G.S.g_mx) &&
+        __float_as_uint(qy) <= __float_as_uint(G.S.g_my) &&
+        __float_as_uint(qz) <= __float_as_uint(G.S.g_mz)) {
       drx = ndrx;
       dry = ndry;
       drz = ndrz;
