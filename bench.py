@@ -296,6 +296,9 @@ def main_ours(args, rank, world, local):
 
     for _ in range(args.warmup):
         step()
+    # determinism evidence: the reduced fixed-point image of a warm-up step and of
+    # the last timed step must be the same integers (checked on rank 0 after the loop)
+    checksum_warm = int(img.sum().item()) if rank == 0 else 0
     sampler = ClockSampler(local)
     barrier()
     sampler.start()
@@ -315,6 +318,7 @@ def main_ours(args, rank, world, local):
         steps_sum = rep["total_steps"]
         rays_local = rep["emitted"]
     clocks = sampler.stop()
+    checksum_last = int(img.sum().item()) if rank == 0 else 0
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -396,7 +400,9 @@ def main_ours(args, rank, world, local):
             "config": dict(workload_config(args, scene, desc, info, world),
                            field_upload_s=field_s, steps_per_ray=steps_sum / max(rays_local, 1)),
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-            "gpu_launches": launches}
+            "gpu_launches": launches,
+            "image_checksum": {"fixed_point_sum": checksum_last,
+                               "identical_to_warmup": checksum_last == checksum_warm}}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
