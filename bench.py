@@ -16,12 +16,17 @@ N GPUs share it).
   e2e         the same image through the public C-ABI with HOST buffers: scene
               sources H2D, render, reduce, FP64 image + per-emitter stats D2H
               (rb_trace at N=1; rb_trace_shard + reduce + rb_image_from_fixed at N>1).
-  roofline    K1 render_emitters against the box's measured FP32 FFMA peak
-              (MEASURED_PEAKS.json has no CUDA-core number; measured here with
-              tools/peaks.cu).  Algorithmic work per ray = 360 flops per RK4 step
-              + 700.
+  roofline    K1 render_emitters against the box's measured FP32 peak (best of
+              FFMA register / immediate / packed FFMA2 forms; MEASURED_PEAKS.json
+              has no CUDA-core number, measured here with tools/peaks.cu).
+              Algorithmic work per ray = 360 flops per RK4 step + 700 (SURVEY.md
+              §8(a)); traffic from the committed ncu capture.
   cpu_baseline  the unmodified reference run_trace (oracle/_ref) on this host's
-              cores, on a bounded random sample of the same emitters.
+              cores, on a bounded random sample of the same emitters (plus the
+              extrapolated whole-image time).
+  gpu_launches  kernels the library launched in the timed steps (its own count).
+  image_checksum  the last timed step's fixed-point image sum, and whether it
+              equals a warm-up step's (bit-reproducibility).
 --impl reference times only that CPU path (rank 0), same metric/config.
 """
 from __future__ import annotations
