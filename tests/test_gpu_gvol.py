@@ -25,7 +25,7 @@ def _grid(name):
 
 
 @pytest.mark.parametrize("name", ["field3d", "shock_particles"])
-@pytest.mark.parametrize("slab_planes", [1, 3, 0])
+@pytest.mark.parametrize("slab_planes", [1, 5, 0])
 def test_gvol_stream_builds_the_reference_grid(tracer, tmp_path, name, slab_planes):
     from paper_1812_05902_b200 import setup as S
     scene, field, grid = _grid(name)
