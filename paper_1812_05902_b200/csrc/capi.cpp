@@ -338,9 +338,10 @@ struct PartialOut {
 // CTAs per emitter (KScene::split).  Splitting an emitter's rays over several
 // CTAs keeps fewer distinct cones in flight, so the cells they read stay in
 // L2; each chunk costs one pilot and one tile flush.  The chunk is sized to
-// about 4e5 RK4 steps, estimating the steps per ray as the box depth along the
-// pupil axis over h (measured optimum: tomo 4-8, bos 16, 1024^3 32; bos +18%,
-// 1024^3 +4%, tomo +1% over one CTA per emitter).  Independently, a work list
+// about 2e5 RK4 steps, estimating the steps per ray as the box depth along the
+// pupil axis over h, halved for emitters inside the box (measured optimum:
+// tomo 4-8, bos 24, 1024^3 flat from 48; bos +20%, 1024^3 +4%, tomo +1% over
+// one CTA per emitter).  Independently, a work list
 // shorter than the resident CTAs is split until every CTA gets two units (3
 // emitters x 4e6 rays: 1.29 s -> 17 ms), never below one patch iteration per
 // unit.  RAYBOS_SPLIT overrides.
@@ -357,8 +358,16 @@ int emitter_split(const rb_ctx* ctx, const rb_scene* s, const rbk::KScene& k, si
     const double an = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
     double depth = 0.0;
     for (int a = 0; a < 3; ++a) depth += std::fabs(ext[a] * ax[a]) / (an > 0.0 ? an : 1.0);
-    const double steps = std::min<double>(depth / k.h, s->max_steps);
-    split = std::min(64.0, std::round(static_cast<double>(s->rays_per_source) * steps / 4e5));
+    // emitters inside the box (Tomo particles) trace half the depth on average
+    int64_t inside = 0;
+    for (int64_t q = 0; q < s->n_sources; ++q) {
+      const rb_vec3 p = s->sources[q];
+      inside += (p.x >= ctx->box_lo.x && p.x <= ctx->box_hi.x && p.y >= ctx->box_lo.y &&
+                 p.y <= ctx->box_hi.y && p.z >= ctx->box_lo.z && p.z <= ctx->box_hi.z);
+    }
+    const double f_in = s->n_sources ? static_cast<double>(inside) / s->n_sources : 0.0;
+    const double steps = std::min<double>(depth / k.h * (1.0 - 0.5 * f_in), s->max_steps);
+    split = std::min(128.0, std::round(static_cast<double>(s->rays_per_source) * steps / 2e5));
   }
   if (n_work > 0 && n_work < static_cast<size_t>(resident_ctas))
     split = std::max(split, std::ceil(2.0 * resident_ctas / static_cast<double>(n_work)));
