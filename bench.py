@@ -269,9 +269,34 @@ def main_ours(args, rank, world, local):
     from paper_1812_05902_b200 import scenes
     from paper_1812_05902_b200.engine import GpuTracer
 
+    # RAYBOS_BENCH_BACKEND=gloo is a path check only: it lets the torchrun
+    # (N>1) code run on a one-GPU box (ranks share the device, collectives go
+    # through host memory); its numbers are not a measurement.
+    backend = os.environ.get("RAYBOS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def reduce_to_root(x):
+        if backend == "nccl":
+            dist.reduce(x, 0)
+        else:
+            h = x.cpu()
+            dist.reduce(h, 0)
+            x.copy_(h)
+
+    def max_over_ranks(x):
+        if backend == "nccl":
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        else:
+            h = x.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX)
+            x.copy_(h)
     tracer = GpuTracer(n_devices=1, first_device=local)
 
     def calibrate(sc):
@@ -296,7 +321,7 @@ def main_ours(args, rank, world, local):
         torch.cuda.current_stream().synchronize()   # the library runs on its own stream
         rep = tracer.trace_shard(scene, True, True, rank, world, img.data_ptr())
         if world > 1:
-            dist.reduce(img, 0)
+            reduce_to_root(img)
         return rep
 
     for _ in range(args.warmup):
@@ -326,7 +351,7 @@ def main_ours(args, rank, world, local):
     checksum_last = int(img.sum().item()) if rank == 0 else 0
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_over_ranks(t)
     ms_per_step = t.item() / args.steps
     value = rays_total / (ms_per_step * 1e-3)
 
@@ -348,14 +373,14 @@ def main_ours(args, rank, world, local):
                 img.zero_()
                 torch.cuda.current_stream().synchronize()
                 tracer.trace_shard(scene, True, True, rank, world, img.data_ptr())
-                dist.reduce(img, 0)
+                reduce_to_root(img)
                 if rank == 0:
                     tracer.image_from_fixed(img.data_ptr(), (H, W))
             barrier()
             e2e_ms.append(1e3 * (time.perf_counter() - s0))
         te = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            max_over_ranks(te)
         e2e = {"value": rays_total / (te.item() * 1e-3), "unit": "rays/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": te.item(),
