@@ -265,7 +265,10 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
   scratch[5] = T0.z;
 
   float drx = 0.f, dry = 0.f, drz = 0.f, dtx = 0.f, dty = 0.f, dtz = 0.f;
-  float pax = q0x, pay = q0y, paz = q0z;  // unperturbed line at xi = step * h
+  // stage-a point (grid units) of the current step: the unperturbed line plus
+  // dr, i.e. the previous step's accepted end point qx = pcx + ndrx (the same
+  // FADD, so carrying it is bit-identical to recomputing pa + dr)
+  float qax = q0x + 0.f, qay = q0y + 0.f, qaz = q0z + 0.f;
   CellPoly cache;
   cache.ox = cache.oy = cache.oz = -1e30f;
   const int max_steps = S.max_steps;
@@ -285,7 +288,7 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
                 pbz = fmaf(az, fs + 0.5f, q0z);
     const float pcx = fmaf(ax, fs + 1.0f, q0x), pcy = fmaf(ay, fs + 1.0f, q0y),
                 pcz = fmaf(az, fs + 1.0f, q0z);
-    const float3 Da = RB_SAMPLE_D(pax + drx, pay + dry, paz + drz);
+    const float3 Da = RB_SAMPLE_D(qax, qay, qaz);
     const float3 Db = RB_SAMPLE_D(fmaf(Da.x, S.kbx, fmaf(dtx, S.hhx, pbx + drx)),
                                fmaf(Da.y, S.kby, fmaf(dty, S.hhy, pby + dry)),
                                fmaf(Da.z, S.kbz, fmaf(dtz, S.hhz, pbz + drz)));
@@ -311,9 +314,9 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
       dtx = ndtx;
       dty = ndty;
       dtz = ndtz;
-      pax = pcx;
-      pay = pcy;
-      paz = pcz;
+      qax = qx;
+      qay = qy;
+      qaz = qz;
       continue;
     }
     if (!(isfinite(ndrx) && isfinite(ndry) && isfinite(ndrz) && isfinite(ndtx) &&
