@@ -4,29 +4,44 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scene tomo]
 
 One JSON line on rank 0.  A step is one full render of the scene's image (all
-emitters, all rays: ray generation -> GRIN RK4 -> optics -> sensor deposition),
-with the emitters sharded over the N ranks and the partial 64-bit fixed-point
-images summed with one NCCL reduce (strong scaling: the 1e9-ray image is fixed,
-N GPUs share it).
+emitters, all rays: ray generation -> GRIN RK4 -> optics -> sensor deposition)
+through the library's public call rb_trace, with the emitters sharded over N
+GPUs and the partial 64-bit fixed-point images summed by the library's own NCCL
+reduce (strong scaling: the 1e9-ray image is fixed, N GPUs share it).
+
+N GPUs, either way the driver launches it:
+  * torchrun --nproc-per-node N bench.py --gpus N: one process per GPU; each
+    rank creates its context with rb_create_rank (rank 0's ncclUniqueId is
+    broadcast over torch.distributed, which is used for nothing else but the
+    barriers and the max-over-ranks of the timings); WORLD_SIZE must equal N.
+  * python bench.py --gpus N: one process drives N GPUs (rb_create(N): one
+    host thread and one NCCL communicator per device) — what the C++ drop-in
+    raybos_gpu::run_trace does on an 8-GPU node.
 
   value       device-resident throughput: density grid resident in HBM, the
-              step = rb_trace_shard (K1 render) + NCCL reduce, timed with CUDA
-              events between barriers, L2 flushed (256 MiB write) before every
-              timed step; max over ranks.
-  e2e         the same image through the public C-ABI with HOST buffers: scene
-              sources H2D, render, reduce, FP64 image + per-emitter stats D2H
-              (rb_trace at N=1; rb_trace_shard + reduce + rb_image_from_fixed at N>1).
-  roofline    K1 render_emitters against the box's measured FP32 peak (best of
-              FFMA register / immediate / packed FFMA2 forms; MEASURED_PEAKS.json
-              has no CUDA-core number, measured here with tools/peaks.cu).
-              Algorithmic work per ray = 360 flops per RK4 step + 700 (SURVEY.md
-              §8(a)); traffic from the committed ncu capture.
+              step = rb_trace leaving the reduced fixed-point image on the
+              device (rb_trace_out.image_fixed; per-source stats, 24 B/source,
+              and counters still come back), L2 flushed (256 MiB write) before
+              every timed step, CUDA events on the launching device around the
+              synchronous call; max over ranks.
+  e2e         the same call with HOST buffers: the FP64 image and the stats
+              copied to the host every step (sources H2D every step in both).
+  roofline    K1 render_emitters: scenes with a medium against the box's
+              measured FP32 FFMA peak (tools/peaks.cu; MEASURED_PEAKS.json
+              has no CUDA-core figure), algorithmic work 360 flops per RK4
+              step + 700 per ray; scenes without a medium
+              against the measured shared-memory RED.ADD throughput, at one
+              RED per pixel of each landed ray's spot window (SURVEY §8(d) rows
+              0 and 3: the deposition binds).  traffic from the committed ncu
+              capture.
   cpu_baseline  the unmodified reference run_trace (oracle/_ref) on this host's
-              cores, on a bounded random sample of the same emitters (plus the
-              extrapolated whole-image time).
+              cores, on a bounded random sample of the same emitters.
   gpu_launches  kernels the library launched in the timed steps (its own count).
   image_checksum  the last timed step's fixed-point image sum, and whether it
               equals a warm-up step's (bit-reproducibility).
+  configs     (N=1 default run) the other BASELINE.json configs — piv, bos,
+              optics and one GPU's 1/8 share of the large 1024^3 image — each
+              with its own value / e2e / roofline / cpu_baseline.
 --impl reference times only that CPU path (rank 0), same metric/config.
 """
 from __future__ import annotations
@@ -50,6 +65,9 @@ METRIC = "rays/sec at 1/2/4/8 B200 for 1e9-ray image through density grid; % of 
 FLOPS_PER_STEP = 360.0
 FLOPS_PER_RAY = 700.0
 GATHER_BYTES_PER_STEP = 384.0
+SCENES = ["piv", "bos", "tomo", "optics", "large"]
+# BASELINE.json configs[i] of each scene
+BASELINE_CONFIG = {"piv": 0, "bos": 1, "tomo": 2, "optics": 3, "large": 4}
 
 
 def dist_env():
@@ -63,8 +81,8 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, indices):
+        self.indices = ",".join(str(i) for i in sorted(set(indices)))
         self.proc = None
         self.path = None
 
@@ -74,7 +92,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
-                 "200", "-i", str(self.index), "-f", self.path],
+                 "200", "-i", self.indices, "-f", self.path],
                 stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -107,19 +125,32 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+_PEAKS = {}
+
+
 def measure_peaks(device: int) -> dict:
+    """The roofline denominators, measured on this box (tools/peaks.cu)."""
+    if device in _PEAKS:
+        return _PEAKS[device]
     from paper_1812_05902_b200 import build as b
     lib = C.CDLL(b.PEAKS_LIB)
-    lib.rbp_ffma_tflops.restype = C.c_double
-    lib.rbp_ffma_tflops.argtypes = [C.c_int, C.c_int]
+    for fn in ("rbp_ffma_tflops",):
+        getattr(lib, fn).restype = C.c_double
+        getattr(lib, fn).argtypes = [C.c_int, C.c_int]
     lib.rbp_l2_gather_gbs.restype = C.c_double
     lib.rbp_l2_gather_gbs.argtypes = [C.c_int, C.c_double]
+    for fn in ("rbp_red_shared_gops", "rbp_dfma_tflops"):
+        getattr(lib, fn).restype = C.c_double
+        getattr(lib, fn).argtypes = [C.c_int]
     reg = lib.rbp_ffma_tflops(device, 0)
     imm = lib.rbp_ffma_tflops(device, 1)
     pk2 = lib.rbp_ffma_tflops(device, 2)   # packed FFMA2, which K1's Horner evaluation uses
-    return {"ffma_reg_tflops": reg, "ffma_imm_tflops": imm, "ffma2_tflops": pk2,
-            "ffma_tflops": max(reg, imm, pk2),
-            "l2_gather_gbs": lib.rbp_l2_gather_gbs(device, 64.0)}
+    _PEAKS[device] = {"ffma_reg_tflops": reg, "ffma_imm_tflops": imm, "ffma2_tflops": pk2,
+                      "ffma_tflops": max(reg, imm, pk2),
+                      "l2_gather_gbs": lib.rbp_l2_gather_gbs(device, 64.0),
+                      "red_shared_gops": lib.rbp_red_shared_gops(device),
+                      "dfma_tflops": lib.rbp_dfma_tflops(device)}
+    return _PEAKS[device]
 
 
 def profiled_traffic(scene: str):
@@ -202,29 +233,49 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scene", default="tomo", choices=["piv", "bos", "tomo", "optics", "large"])
-    ap.add_argument("--scale", type=float, default=1.0, help="emitter-count scale (tests only)")
+    ap.add_argument("--scene", default="tomo", choices=SCENES)
+    ap.add_argument("--scale", type=float, default=None,
+                    help="emitter-count scale (default 1; 'large' defaults to 1/8 = one GPU's "
+                         "share of the 8-GPU image)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra-configs", action="store_true",
+                    help="N=1: skip the other four BASELINE configs")
     args = ap.parse_args()
     rank, world, local = dist_env()
+    if world > 1 and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; launch one rank per GPU",
+              file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return main_reference(args, rank, world)
     return main_ours(args, rank, world, local)
 
 
-def workload_config(args, scene, desc, info, world):
-    return {"workload": f"{args.scene}: {scene.n_sources} emitters x {scene.rays_per_source} rays "
-                        f"({scene.n_sources * scene.rays_per_source:.3g} rays/image), "
+def default_scale(name, scale):
+    if scale is not None:
+        return scale
+    return 0.125 if name == "large" else 1.0
+
+
+def workload_config(name, scene, desc, info, n_gpus):
+    share = ""
+    if name == "large":
+        share = (f" (one GPU's 1/8 share of the {8 * scene.n_sources} x "
+                 f"{scene.rays_per_source} = {8 * scene.n_sources * scene.rays_per_source:.3g}-ray "
+                 "8-GPU image)")
+    return {"workload": f"{name}: {scene.n_sources} emitters x {scene.rays_per_source} rays "
+                        f"({scene.n_sources * scene.rays_per_source:.3g} rays/image){share}, "
                         f"{scene.width}x{scene.height} sensor" +
                         (f", {desc['field']}" if "field" in desc else ", no medium"),
-            "scene": args.scene, "emitters": scene.n_sources,
+            "baseline_config": BASELINE_CONFIG[name],
+            "scene": name, "emitters": scene.n_sources,
             "rays_per_emitter": scene.rays_per_source,
-            "rays_per_step": scene.n_sources * scene.rays_per_source,
+            "rays_per_image": scene.n_sources * scene.rays_per_source,
             "sensor": [scene.width, scene.height], "delta_xi_m": scene.delta_xi,
             "d_tau_m": scene.d_tau, "magnification": info.magnification,
-            "parallelism": f"emitter shards x{world}, NCCL reduce of int64 image",
+            "parallelism": f"emitter shards x{n_gpus}, NCCL reduce of int64 image",
             "l2": "256 MiB L2 flush before every timed step"}
 
 
@@ -238,7 +289,8 @@ def main_reference(args, rank, world):
     def calibrate(sc):
         return orc.trace(sc, None, with_field=False, accumulate_image=True).image
 
-    scene, grid, info, desc = scenes.build(args.scene, calibrate=calibrate, scale=args.scale)
+    scale = default_scale(args.scene, args.scale)
+    scene, grid, info, desc = scenes.build(args.scene, calibrate=calibrate, scale=scale)
     run, m, kind, thr = cpu_reference(scene, grid, args.cpu_seconds)
     for _ in range(args.warmup):
         run(max(1, m // 8))
@@ -248,12 +300,15 @@ def main_reference(args, rank, world):
         ts.append(t)
     rays = m * scene.rays_per_source
     value = rays / (sum(ts) / len(ts))
-    cfg = workload_config(args, scene, desc, info, world)
+    cfg = workload_config(args.scene, scene, desc, info, args.gpus)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sum(ts) / len(ts), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": cfg,
+            # what one timed step actually traced: a random sample of the
+            # workload's emitters (the rate is unbiased; the image is not whole)
+            "timed_rays_per_step": rays, "timed_emitters_per_step": m,
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": thr, "kind": kind,
                              "sample": f"{m} of {scene.n_sources} emitters x "
                                        f"{scene.rays_per_source} rays per step"},
@@ -263,180 +318,246 @@ def main_reference(args, rank, world):
     return 0
 
 
-def main_ours(args, rank, world, local):
-    import torch
-    import torch.distributed as dist
+class Job:
+    """The process's place in the N-GPU job and its collectives (timing only)."""
+
+    def __init__(self, args, rank, world, local):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank, self.world, self.gpus = rank, world, args.gpus
+        # RAYBOS_BENCH_BACKEND=gloo is a path check only: it lets the torchrun
+        # (N>1) code run on a one-GPU box (ranks share the device, the library's
+        # NCCL replaced by tests/fake_nccl through RAYBOS_NCCL_LIB); its
+        # numbers are not a measurement.
+        self.backend = os.environ.get("RAYBOS_BENCH_BACKEND", "nccl")
+        ndev = torch.cuda.device_count()
+        self.device = local if self.backend == "nccl" else local % ndev
+        torch.cuda.set_device(self.device)
+        from paper_1812_05902_b200.engine import GpuTracer, nccl_unique_id
+        if world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+            else:
+                dist.init_process_group(self.backend)
+            uid = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            self.tracer = GpuTracer.for_rank(self.device, rank, world, uid[0])
+            self.devices = [self.device]
+        elif args.gpus > 1:
+            # RAYBOS_BENCH_DEVICES (path check only, e.g. "0,0" on a one-GPU box
+            # with the NCCL stand-in) names the devices; default 0..N-1
+            env = os.environ.get("RAYBOS_BENCH_DEVICES")
+            self.devices = ([int(x) for x in env.split(",")] if env else list(range(args.gpus)))
+            assert len(self.devices) == args.gpus
+            self.tracer = GpuTracer(devices=self.devices)
+        else:
+            self.tracer = GpuTracer(n_devices=1, first_device=self.device)
+            self.devices = [self.device]
+        self.comm = self.tracer.comm_info()
+        print(f"raybos: rank {rank} of {world} process(es), devices {self.devices}, NCCL "
+              f"communicator spans {self.comm['comm_ranks']} rank(s)"
+              f" (NCCL version code {self.comm['nccl_version']})", file=sys.stderr, flush=True)
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        for d in sorted(set(self.devices)):
+            self.torch.cuda.synchronize(d)
+
+    def max_over_ranks(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64,
+                              device="cuda" if self.backend == "nccl" else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        self.tracer.close()
+        if self.world > 1:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+def spot_reds_per_ray(scene):
+    """Shared-memory REDs per landed ray of the deposition: the spot window is
+    floor(c + hw) - floor(c - hw) + 1 pixels a side (sensor.cpp:44-55), i.e.
+    2 hw + 1 on average over sub-pixel centres."""
+    sigma = 0.25 * scene.d_tau
+    hw = scene.sensor.window_sigmas * sigma / scene.sensor.pitch
+    if sigma < 1e-3 * scene.sensor.pitch:
+        return 1.0
+    return (2.0 * hw + 1.0) ** 2
+
+
+def bench_scene(job, name, scale, steps, warmup, args, want_cpu, want_e2e):
+    """One BASELINE config through rb_trace; returns the JSON entry (rank 0)."""
+    torch = job.torch
     from paper_1812_05902_b200 import scenes
-    from paper_1812_05902_b200.engine import GpuTracer
+    tracer = job.tracer
 
-    # RAYBOS_BENCH_BACKEND=gloo is a path check only: it lets the torchrun
-    # (N>1) code run on a one-GPU box (ranks share the device, collectives go
-    # through host memory); its numbers are not a measurement.
-    backend = os.environ.get("RAYBOS_BENCH_BACKEND", "nccl")
-    if backend != "nccl":
-        local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+    def calibrate(sc):  # the gain-calibration dot (engine.cpp:396-412); image on rank 0 only
+        img = tracer.run_trace(sc, with_field=False, accumulate_image=True, host_image=True).image
+        return img if img is not None else np.zeros(1)
 
-    def reduce_to_root(x):
-        if backend == "nccl":
-            dist.reduce(x, 0)
-        else:
-            h = x.cpu()
-            dist.reduce(h, 0)
-            x.copy_(h)
-
-    def max_over_ranks(x):
-        if backend == "nccl":
-            dist.all_reduce(x, op=dist.ReduceOp.MAX)
-        else:
-            h = x.cpu()
-            dist.all_reduce(h, op=dist.ReduceOp.MAX)
-            x.copy_(h)
-    tracer = GpuTracer(n_devices=1, first_device=local)
-
-    def calibrate(sc):
-        return tracer.run_trace(sc, with_field=False, accumulate_image=True).image
-
-    scene, grid, info, desc = scenes.build(args.scene, calibrate=calibrate, scale=args.scale)
+    scene, grid, info, desc = scenes.build(name, calibrate=calibrate, scale=scale)
     t0 = time.perf_counter()
     tracer.set_field(grid)
     field_s = time.perf_counter() - t0
     W, H = scene.width, scene.height
     rays_total = scene.n_sources * scene.rays_per_source
-    img = torch.zeros(W * H, dtype=torch.int64, device="cuda")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+    dev0 = job.devices[0]
+    img = torch.zeros(W * H, dtype=torch.int64, device=f"cuda:{dev0}") if job.rank == 0 else None
+    flush = [torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{d}")
+             for d in sorted(set(job.devices))]
 
     def step():
-        img.zero_()
-        torch.cuda.current_stream().synchronize()   # the library runs on its own stream
-        rep = tracer.trace_shard(scene, True, True, rank, world, img.data_ptr())
-        if world > 1:
-            reduce_to_root(img)
-        return rep
+        return tracer.run_trace(scene, True, True, host_image=False,
+                                image_fixed_ptr=img.data_ptr() if img is not None else 0)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
-    # determinism evidence: the reduced fixed-point image of a warm-up step and of
-    # the last timed step must be the same integers (checked on rank 0 after the loop)
-    checksum_warm = int(img.sum().item()) if rank == 0 else 0
-    sampler = ClockSampler(local)
-    barrier()
+    checksum_warm = int(img.sum().item()) if img is not None else 0
+    sampler = ClockSampler(job.devices)
+    job.barrier()
     sampler.start()
     time.sleep(0.3)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    total_ms, kernel_ms, steps_sum, rays_local, launches = 0.0, [], 0, 0, 0
-    for k in range(args.steps):
-        flush.fill_(k & 0xFF)
-        barrier()
-        ev0.record()
-        rep = step()
-        ev1.record()
-        torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev0)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    total_ms, kernel_ms, launches, res = 0.0, [], 0, None
+    for k in range(steps):
+        for f in flush:
+            f.fill_(k & 0xFF)
+        job.barrier()
+        with torch.cuda.device(dev0):
+            ev0.record(stream)
+            res = step()
+            ev1.record(stream)
+        torch.cuda.synchronize(dev0)
         total_ms += ev0.elapsed_time(ev1)
-        kernel_ms.append(rep["kernel_ms"])
-        launches += rep["kernel_launches"]  # render + split-stats kernels (library count)
-        steps_sum = rep["total_steps"]
-        rays_local = rep["emitted"]
+        kernel_ms.append(res.report["kernel_ms"])
+        launches += res.report["kernel_launches"]
     clocks = sampler.stop()
-    checksum_last = int(img.sum().item()) if rank == 0 else 0
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        max_over_ranks(t)
-    ms_per_step = t.item() / args.steps
+    checksum_last = int(img.sum().item()) if img is not None else 0
+    ms_per_step = job.max_over_ranks(total_ms / steps)
+    kms = job.max_over_ranks(sum(kernel_ms) / len(kernel_ms))
     value = rays_total / (ms_per_step * 1e-3)
+    steps_sum = res.report["total_steps"]          # whole call (all ranks, all devices)
 
-    # e2e through the public C-ABI with host buffers
     e2e = None
-    if not args.no_e2e:
+    if want_e2e:
         n_src = scene.n_sources
         h2d = n_src * (3 * 8 + 4)                  # source positions + work order
         d2h = W * H * 8 + n_src * (2 * 8 + 8) + 6 * 8   # FP64 image + stats + counters
-        if world == 1:
-            tracer.run_trace(scene, True, True)
         e2e_ms = []
-        for _ in range(args.steps):
-            barrier()
+        tracer.run_trace(scene, True, True, host_image=(job.rank == 0))
+        for _ in range(steps):
+            job.barrier()
             s0 = time.perf_counter()
-            if world == 1:
-                tracer.run_trace(scene, True, True)
-            else:
-                img.zero_()
-                torch.cuda.current_stream().synchronize()
-                tracer.trace_shard(scene, True, True, rank, world, img.data_ptr())
-                reduce_to_root(img)
-                if rank == 0:
-                    tracer.image_from_fixed(img.data_ptr(), (H, W))
-            barrier()
+            tracer.run_trace(scene, True, True, host_image=(job.rank == 0))
+            job.barrier()
             e2e_ms.append(1e3 * (time.perf_counter() - s0))
-        te = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            max_over_ranks(te)
-        e2e = {"value": rays_total / (te.item() * 1e-3), "unit": "rays/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": te.item(),
-               "path": "rb_trace (C-ABI, host buffers)" if world == 1 else
-                       "rb_trace_shard + NCCL reduce + rb_image_from_fixed (host buffers)"}
+        te = job.max_over_ranks(sum(e2e_ms) / len(e2e_ms))
+        e2e = {"value": rays_total / (te * 1e-3), "unit": "rays/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": te,
+               "path": "rb_trace (C-ABI, host buffers)"}
+    if job.rank != 0:
+        return None
 
-    if rank != 0:
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return 0
-
-    peaks = measure_peaks(local)
-    kms = sum(kernel_ms) / len(kernel_ms)
-    flops = FLOPS_PER_STEP * steps_sum + FLOPS_PER_RAY * rays_local
-    achieved = flops / (kms * 1e-3) / 1e12
-    gather = GATHER_BYTES_PER_STEP * steps_sum / (kms * 1e-3) / 1e9
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": peaks["ffma_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["ffma_tflops"],
-                "traffic": profiled_traffic(args.scene) if world == 1 else None,
-                "traffic_source": "profiles/k1_traffic.json (ncu --set full, one launch)",
-                "kernel": "render_emitters", "kernel_ms": kms,
-                "peak_source": "measured on this box: FFMA microbenchmark (tools/peaks.cu), "
-                               "max of register / immediate / packed-FFMA2 forms",
-                "per_ray": f"{FLOPS_PER_STEP:.0f} flops/RK4 step + {FLOPS_PER_RAY:.0f}; "
-                           f"{steps_sum / max(rays_local, 1):.1f} steps/ray measured",
-                # what the samples would move if each gathered its 8 corners
-                # (3 x 8 x 16 B per step): above the measured L2 gather peak,
-                # which is why K1 caches the cell in registers instead
-                "gather": {"uncached_equivalent_gbs": gather,
-                           "l2_gather_peak_gbs": peaks["l2_gather_gbs"],
-                           "bytes_per_step": GATHER_BYTES_PER_STEP},
-                "ffma_reg_tflops": peaks["ffma_reg_tflops"],
-                "ffma_imm_tflops": peaks["ffma_imm_tflops"],
-                "ffma2_tflops": peaks["ffma2_tflops"], "hbm_gbs_measured": measured_hbm()}
+    peaks = measure_peaks(dev0)
+    n_gpus = len(job.devices) * job.world
+    if grid is not None:
+        flops = FLOPS_PER_STEP * steps_sum + FLOPS_PER_RAY * rays_total
+        achieved = flops / n_gpus / (kms * 1e-3) / 1e12
+        gather = GATHER_BYTES_PER_STEP * steps_sum / n_gpus / (kms * 1e-3) / 1e9
+        roofline = {"bound": "fp32", "achieved": achieved, "peak": peaks["ffma_tflops"],
+                    "unit": "TFLOP/s", "frac": achieved / peaks["ffma_tflops"],
+                    "per_ray": f"{FLOPS_PER_STEP:.0f} flops/RK4 step + {FLOPS_PER_RAY:.0f}; "
+                               f"{steps_sum / max(rays_total, 1):.1f} steps/ray measured",
+                    "peak_source": "measured on this box: FFMA microbenchmark "
+                                   "(tools/peaks.cu), max of register / immediate / packed-FFMA2",
+                    # what the samples would move if each gathered its 8 corners
+                    # (3 x 8 x 16 B per step): above the measured L2 gather peak,
+                    # which is why K1 caches the cell in registers instead
+                    "gather": {"uncached_equivalent_gbs": gather,
+                               "l2_gather_peak_gbs": peaks["l2_gather_gbs"],
+                               "bytes_per_step": GATHER_BYTES_PER_STEP}}
+    else:
+        landed = res.report["landed"]
+        reds = spot_reds_per_ray(scene) * landed
+        achieved = reds / n_gpus / (kms * 1e-3) / 1e9
+        roofline = {"bound": "smem_red", "achieved": achieved, "peak": peaks["red_shared_gops"],
+                    "unit": "Gop/s", "frac": achieved / peaks["red_shared_gops"],
+                    "per_ray": f"{spot_reds_per_ray(scene):.1f} shared-memory RED.ADD.U32 per "
+                               f"landed ray (spot window (2 hw + 1)^2); {landed} of "
+                               f"{rays_total} rays landed",
+                    "peak_source": "measured on this box: conflict-free red.shared.add.u32 "
+                                   "microbenchmark (tools/peaks.cu)",
+                    "fp32_tflops_equivalent": (FLOPS_PER_RAY * rays_total / n_gpus /
+                                               (kms * 1e-3) / 1e12)}
+    roofline.update({"traffic": profiled_traffic(name) if n_gpus == 1 else None,
+                     "traffic_source": "profiles/k1_traffic.json (ncu --set full, one launch)",
+                     "kernel": "render_emitters", "kernel_ms": kms,
+                     "ffma_reg_tflops": peaks["ffma_reg_tflops"],
+                     "ffma_imm_tflops": peaks["ffma_imm_tflops"],
+                     "ffma2_tflops": peaks["ffma2_tflops"],
+                     "red_shared_gops": peaks["red_shared_gops"],
+                     "dfma_tflops": peaks["dfma_tflops"],
+                     "hbm_gbs_measured": measured_hbm(), "peak_clocks": clocks})
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if want_cpu:
         try:
             cpu = cpu_baseline_entry(scene, grid, args.cpu_seconds)
         except Exception as e:  # report, never hide
             cpu = {"value": None, "unit": "rays/s", "cores": None, "kind": "reference",
                    "sample": f"failed: {e}"}
-    line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 GRIN + f64 raygen/optics/sensor", "data": "synthetic",
-            "config": dict(workload_config(args, scene, desc, info, world),
-                           field_upload_s=field_s, steps_per_ray=steps_sum / max(rays_local, 1)),
+    return {"value": value, "ms_per_step": ms_per_step, "steps": steps, "warmup": warmup,
+            "config": workload_config(name, scene, desc, info, n_gpus),
+            "setup": {"field_upload_s": field_s,
+                      "steps_per_ray": steps_sum / max(rays_total, 1)},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": launches,
             "image_checksum": {"fixed_point_sum": checksum_last,
                                "identical_to_warmup": checksum_last == checksum_warm}}
-    print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+
+
+def main_ours(args, rank, world, local):
+    job = Job(args, rank, world, local)
+    n_gpus = len(job.devices) * job.world
+    single = n_gpus == 1
+    head = bench_scene(job, args.scene, default_scale(args.scene, args.scale), args.steps,
+                       args.warmup, args, want_cpu=single and not args.no_cpu_baseline,
+                       want_e2e=not args.no_e2e)
+    extras = {}
+    if single and not args.no_extra_configs and args.scene == "tomo" and args.scale is None:
+        # the other BASELINE configs, at a few steps each (inside the default run)
+        for name in ("piv", "bos", "optics", "large"):
+            try:
+                e = bench_scene(job, name, default_scale(name, None), min(args.steps, 3),
+                                max(3, min(args.warmup, 3)), args,
+                                want_cpu=not args.no_cpu_baseline, want_e2e=not args.no_e2e)
+            except Exception as ex:  # report, never hide
+                e = {"error": f"{type(ex).__name__}: {ex}"}
+            extras[name] = e
+            job.tracer.set_field(None)
+    if rank == 0:
+        line = {"metric": METRIC, "value": head["value"], "unit": "rays/s", "n_gpus": n_gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32 GRIN + f64 raygen/optics/sensor", "data": "synthetic",
+                "config": head["config"], "setup": head["setup"], "e2e": head["e2e"],
+                "roofline": head["roofline"], "cpu_baseline": head["cpu_baseline"],
+                "clocks": head["clocks"], "gpu_launches": head["gpu_launches"],
+                "image_checksum": head["image_checksum"],
+                "comm": dict(job.comm, mode=("ranks" if job.world > 1 else
+                                             ("in-process" if n_gpus > 1 else "single")),
+                             processes=job.world, devices_per_process=len(job.devices))}
+        if extras:
+            line["configs"] = extras
+        print(json.dumps(line), flush=True)
+    job.close()
     return 0
 
 

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define RB_ABI_VERSION 1
+#define RB_ABI_VERSION 2
 
 /* ---- status codes ------------------------------------------------------- */
 #define RB_OK 0
@@ -169,14 +169,42 @@ typedef struct rb_trace_out {
   double gain;
   int32_t bit_depth;
   int32_t kernel_launches; /* out: CUDA kernels this call launched (all devices) */
+  /* optional device-resident result (ABI 2): when non-NULL and accumulate_image
+   * is set, the reduced fixed-point image (W*H uint64, radiance * 2^31, the
+   * integer ImageBuffer before rb_image_from_fixed's conversion) is left in
+   * this DEVICE buffer, which lives on the context's first device (rank 0 in
+   * rank mode); `image` and `quantized` may then be NULL to skip host copies. */
+  uint64_t* image_fixed;
 } rb_trace_out;
 
 typedef struct rb_ctx rb_ctx;
 
 /* ---- lifecycle ---------------------------------------------------------- */
 /* n_devices <= 0: all visible devices.  first_device: ordinal of the first
- * device to use (devices first_device .. first_device+n-1). */
+ * device to use (devices first_device .. first_device+n-1).  With more than one
+ * device the context renders on all of them from this process (one host thread
+ * per device) and owns one NCCL communicator per device (ncclCommInitAll):
+ * this is what raybos::run_trace's worker pool (engine.cpp:442-490) becomes on
+ * an 8-GPU node.  NCCL is dlopen'ed (libnccl.so.2; RAYBOS_NCCL_LIB overrides). */
 int rb_create(int n_devices, int first_device, rb_ctx** out, char* err, size_t errlen);
+/* The same over an explicit list of device ordinals. */
+int rb_create_devices(const int* devices, int n_devices, rb_ctx** out, char* err, size_t errlen);
+
+/* ---- one process per GPU (torchrun / MPI style launchers) --------------- */
+/* rank 0 creates the communicator id and hands the bytes to the other ranks
+ * (any out-of-band channel, e.g. a torch.distributed broadcast); every rank then
+ * calls rb_create_rank.  In a rank context rb_trace / rb_trace_bos_pair trace
+ * this rank's shard of the SAME scene (all ranks pass the same scene), the
+ * library sums the partial images onto rank 0 with one ncclReduce and
+ * all-reduces the per-source stats and counters, so every rank returns the
+ * whole call's DotHitStats and RunReport and rank 0 also returns the image. */
+#define RB_NCCL_UNIQUE_ID_BYTES 128
+int rb_nccl_unique_id(void* id, size_t len, char* err, size_t errlen);
+int rb_create_rank(int device, int rank, int world, const void* id, size_t len, rb_ctx** out,
+                   char* err, size_t errlen);
+/* This context's place in the job: rank/world (1 unless rank mode), the number
+ * of ranks its NCCL communicator spans (1 without one) and NCCL's version code. */
+int rb_comm_info(const rb_ctx* ctx, int* rank, int* world, int* comm_ranks, int* nccl_version);
 void rb_destroy(rb_ctx* ctx);
 const char* rb_last_error(const rb_ctx* ctx);
 int rb_abi_version(void);
@@ -210,9 +238,12 @@ int64_t rb_field_bytes(const rb_ctx* ctx);
 
 /* ---- the hot path -------------------------------------------------------- */
 /* run_trace(setup, with_field, accumulate_image, run).  Sources are split over
- * the context's devices; the partial fixed-point images are summed with one
- * NCCL reduce when more than one device is used.  Bit-identical results for
- * any device count. */
+ * the context's devices (and ranks); the partial fixed-point images are summed
+ * with one NCCL reduce when more than one device takes part, and every device
+ * takes part in it, including those whose shard is empty.  Bit-identical
+ * results for any device count.  Fails with RB_E_RUNTIME, rather than
+ * returning a wrapped sum, if a landed ray's sensor-plane coordinate exceeds
+ * the fixed-point range of hit_sum (2^22 m / rays_per_source). */
 int rb_trace(rb_ctx* ctx, const rb_scene* scene, int with_field, int accumulate_image,
              rb_trace_out* out);
 

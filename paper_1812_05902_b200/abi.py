@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-RB_ABI_VERSION = 1
+RB_ABI_VERSION = 2
 RB_OK, RB_E_INVALID, RB_E_RUNTIME, RB_E_CUDA, RB_E_NODEVICE = 0, 1, 2, 3, 4
 RB_RAY_LANDED, RB_RAY_LOST, RB_RAY_APERTURE, RB_RAY_MISSED, RB_RAY_TIR, RB_RAY_SENSOR_MISS = range(6)
 RB_ELEM_APERTURE, RB_ELEM_SINGLET, RB_ELEM_THIN_LENS, RB_ELEM_MIRROR = range(4)
@@ -65,7 +65,8 @@ class TraceOut(C.Structure):
                 ("wall_seconds", C.c_double), ("threads", C.c_int32), ("reserved", C.c_int32),
                 ("config_hash", C.c_uint64), ("total_steps", C.c_int64),
                 ("kernel_ms", C.c_double), ("quantized", C.POINTER(C.c_uint16)),
-                ("gain", C.c_double), ("bit_depth", C.c_int32), ("kernel_launches", C.c_int32)]
+                ("gain", C.c_double), ("bit_depth", C.c_int32), ("kernel_launches", C.c_int32),
+                ("image_fixed", C.c_void_p)]
 
 
 def vec3(v) -> Vec3:
@@ -107,8 +108,10 @@ EXPORTED_SYMBOLS = (
     "rb_set_field_nodes", "rb_set_field_density", "rb_clear_field", "rb_field_bytes",
     "rb_trace", "rb_plan_shards", "rb_trace_shard", "rb_image_from_fixed", "rb_trace_rays",
     "rb_trace_rays_fp64", "rb_trace_stats_fp64", "rb_trace_debug", "rb_trace_bos_pair",
-    "rb_set_field_gvol",
+    "rb_set_field_gvol", "rb_create_devices", "rb_nccl_unique_id", "rb_create_rank",
+    "rb_comm_info",
 )
+RB_NCCL_UNIQUE_ID_BYTES = 128
 
 _lib = None
 
@@ -127,6 +130,15 @@ def load_library(path: str | None = None) -> C.CDLL:
     ctx_pp = C.POINTER(C.c_void_p)
     lib.rb_create.argtypes = [C.c_int, C.c_int, ctx_pp, C.c_char_p, C.c_size_t]
     lib.rb_create.restype = C.c_int
+    lib.rb_create_devices.argtypes = [C.POINTER(C.c_int), C.c_int, ctx_pp, C.c_char_p, C.c_size_t]
+    lib.rb_create_devices.restype = C.c_int
+    lib.rb_nccl_unique_id.argtypes = [C.c_void_p, C.c_size_t, C.c_char_p, C.c_size_t]
+    lib.rb_nccl_unique_id.restype = C.c_int
+    lib.rb_create_rank.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_size_t, ctx_pp,
+                                   C.c_char_p, C.c_size_t]
+    lib.rb_create_rank.restype = C.c_int
+    lib.rb_comm_info.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 4
+    lib.rb_comm_info.restype = C.c_int
     lib.rb_destroy.argtypes = [C.c_void_p]
     lib.rb_destroy.restype = None
     lib.rb_last_error.argtypes = [C.c_void_p]

@@ -78,6 +78,19 @@ def build_peaks(verbose: bool = False) -> str:
     return PEAKS_LIB
 
 
+FAKE_NCCL_SRC = os.path.join(ROOT, "tests", "fake_nccl", "fake_nccl.cpp")
+FAKE_NCCL_LIB = os.path.join(ROOT, "tests", "fake_nccl", "libfakenccl.so")
+
+
+def build_fake_nccl(verbose: bool = False) -> str:
+    """Test infrastructure: the host-staged NCCL stand-in that lets the
+    library's multi-GPU paths run on a one-GPU box (RAYBOS_NCCL_LIB)."""
+    if _stale(FAKE_NCCL_LIB, [FAKE_NCCL_SRC]):
+        _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-x", "c++",
+              FAKE_NCCL_SRC, "-o", FAKE_NCCL_LIB, "-Wno-deprecated-gpu-targets"], verbose)
+    return FAKE_NCCL_LIB
+
+
 def build_oracle(verbose: bool = False) -> None:
     """Builds oracle/liboracle.so and, where /root/reference exists, oracle/_ref."""
     out = _run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"], verbose)
@@ -89,4 +102,5 @@ if __name__ == "__main__":
     v = "-v" in sys.argv
     print(build_library(verbose=v, force="--force" in sys.argv))
     print(build_peaks(verbose=v))
+    print(build_fake_nccl(verbose=v))
     build_oracle(verbose=v)

@@ -33,21 +33,49 @@ namespace {
 
 constexpr int kShardTile = 32;  // consecutive (Z-ordered) sources per shard tile
 
+// Device allocation owned by one Device (move-only; freed on destruction, on
+// the device it was allocated on), so early error returns cannot leak it.
 struct Buf {
   void* p = nullptr;
   size_t cap = 0;
+  int dev = -1;
+  Buf() = default;
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  Buf(Buf&& o) noexcept : p(o.p), cap(o.cap), dev(o.dev) {
+    o.p = nullptr;
+    o.cap = 0;
+  }
+  Buf& operator=(Buf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      cap = o.cap;
+      dev = o.dev;
+      o.p = nullptr;
+      o.cap = 0;
+    }
+    return *this;
+  }
+  ~Buf() { release(); }
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
+    release();
     const size_t want = std::max<size_t>(bytes, 256);
+    cudaGetDevice(&dev);
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) cap = want;
+    else p = nullptr;
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (dev >= 0 && dev != cur) cudaSetDevice(dev);
+      cudaFree(p);
+      if (dev >= 0 && dev != cur && cur >= 0) cudaSetDevice(cur);
+    }
     p = nullptr;
     cap = 0;
   }
@@ -76,27 +104,47 @@ struct Device {
   Buf hit_part, landed_part, hit_part0, landed_part0;  // split-emitter partials
 };
 
+// NCCL, dlopen'ed on first multi-GPU use (libnccl.so.2 — the copy torch has
+// already loaded, or the system one; RAYBOS_NCCL_LIB overrides the path, which
+// the tests use to substitute a host-staged stand-in on a one-GPU box).
 struct NcclApi {
   void* h = nullptr;
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
   decltype(&ncclCommInitAll) init_all = nullptr;
+  decltype(&ncclCommInitRank) init_rank = nullptr;
   decltype(&ncclReduce) reduce = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclCommCount) count = nullptr;
+  decltype(&ncclGetVersion) version = nullptr;
   bool load(std::string& err) {
     if (h) return true;
-    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    const char* path = std::getenv("RAYBOS_NCCL_LIB");
+    if (!path || !*path) path = "libnccl.so.2";
+    h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
     if (!h) {
-      err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      err = std::string("cannot load ") + path + ": " + dlerror();
       return false;
     }
-    init_all = reinterpret_cast<decltype(init_all)>(dlsym(h, "ncclCommInitAll"));
-    reduce = reinterpret_cast<decltype(reduce)>(dlsym(h, "ncclReduce"));
-    group_start = reinterpret_cast<decltype(group_start)>(dlsym(h, "ncclGroupStart"));
-    group_end = reinterpret_cast<decltype(group_end)>(dlsym(h, "ncclGroupEnd"));
-    destroy = reinterpret_cast<decltype(destroy)>(dlsym(h, "ncclCommDestroy"));
-    if (!init_all || !reduce || !group_start || !group_end || !destroy) {
-      err = "libnccl.so.2 lacks required symbols";
+#define RB_SYM(field, name) field = reinterpret_cast<decltype(field)>(dlsym(h, name))
+    RB_SYM(get_unique_id, "ncclGetUniqueId");
+    RB_SYM(init_all, "ncclCommInitAll");
+    RB_SYM(init_rank, "ncclCommInitRank");
+    RB_SYM(reduce, "ncclReduce");
+    RB_SYM(all_reduce, "ncclAllReduce");
+    RB_SYM(group_start, "ncclGroupStart");
+    RB_SYM(group_end, "ncclGroupEnd");
+    RB_SYM(destroy, "ncclCommDestroy");
+    RB_SYM(count, "ncclCommCount");
+    RB_SYM(version, "ncclGetVersion");
+#undef RB_SYM
+    if (!get_unique_id || !init_all || !init_rank || !reduce || !all_reduce || !group_start ||
+        !group_end || !destroy || !count || !version) {
+      err = std::string(path) + " lacks required NCCL symbols";
+      dlclose(h);
+      h = nullptr;
       return false;
     }
     return true;
@@ -107,19 +155,28 @@ struct NcclApi {
 
 struct rb_ctx {
   std::vector<Device> devs;
+  std::mutex err_mu;  // fail() may run on several device threads at once
   std::string last_error;
   bool has_field = false;
   bool has_field64 = false;  // FP64 node copy present (grids <= RB_FP64_MAX_NODES)
   rb_field_desc field{};
   double3 box_lo{}, box_hi{};
   NcclApi nccl;
+  // Multi-GPU.  In-process: one communicator per device (ncclCommInitAll).
+  // Rank mode (one process per GPU, rb_create_rank): one device, one
+  // communicator, and this process renders shard `rank` of `world`.  Either
+  // way every device of every process takes part in every collective.
   std::vector<ncclComm_t> comms;
+  int rank = 0, world = 1;
 };
 
 namespace {
 
 int fail(rb_ctx* ctx, int code, const std::string& msg, char* err = nullptr, size_t len = 0) {
-  if (ctx) ctx->last_error = msg;
+  if (ctx) {
+    std::lock_guard<std::mutex> lk(ctx->err_mu);
+    ctx->last_error = msg;
+  }
   if (err && len) {
     std::strncpy(err, msg.c_str(), len - 1);
     err[len - 1] = '\0';
@@ -272,6 +329,7 @@ rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, in
   k.half_width = se.window_sigmas * k.sigma / se.pitch;        // sensor.cpp:79
   k.inv_s = 1.0 / (k.sigma * 1.41421356237309504880 / se.pitch);  // sensor.cpp:86
   k.degenerate = k.sigma < 1e-3 * se.pitch ? 1 : 0;              // sensor.cpp:71
+  k.hit_limit = std::ldexp(1.0, 22) / std::max(1, s->rays_per_source);  // render.cuh add_hit
   k.accumulate = accumulate ? 1 : 0;
   return k;
 }
@@ -332,7 +390,8 @@ struct PartialOut {
   unsigned long long counters0[6] = {0, 0, 0, 0, 0, 0};
   float ms = 0.f;
   int err_flag = 0;
-  int launches = 0;  // kernels render_on launched
+  int launches = 0;  // kernels launch_on launched
+  bool pair = false;
 };
 
 // CTAs per emitter (KScene::split).  Splitting an emitter's rays over several
@@ -386,14 +445,36 @@ cudaError_t join_default_stream(Device& dev) {
   return cudaStreamWaitEvent(dev.stream, dev.ev_join, 0);
 }
 
-int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& base,
-              const std::vector<int32_t>& work, unsigned long long* image_target,
+// Runs fn(dev) for every device of the context, each on its own host thread
+// when there are several (field builds of a 1024^3 grid take ~1 s per device,
+// so N devices build in parallel rather than in N seconds).
+template <typename F>
+int for_each_device(rb_ctx* ctx, F&& fn) {
+  const size_t nd = ctx->devs.size();
+  if (nd == 1) return fn(ctx->devs[0]);
+  std::vector<int> rcs(nd, RB_OK);
+  std::vector<std::thread> pool;
+  for (size_t i = 0; i < nd; ++i) pool.emplace_back([&, i] { rcs[i] = fn(ctx->devs[i]); });
+  for (auto& t : pool) t.join();
+  for (int rc : rcs)
+    if (rc) return rc;
+  return RB_OK;
+}
+
+// Phase 1 of a render on one device: uploads, zeroing, K1 (+ the split-stats
+// kernel), all queued on the device's stream.  image_target: a caller-owned
+// device image to accumulate into instead of the device's own (zeroed) one.
+// zero_stats: also zero the per-source stats, so entries this device does not
+// own are 0 rather than stale (rank mode sums them across processes).
+int launch_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& base,
+              const std::vector<int32_t>& work, unsigned long long* image_target, bool zero_stats,
               PartialOut& po) {
   RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
   const int64_t n = s->n_sources;
   const size_t npx = static_cast<size_t>(s->sensor.width_px) * s->sensor.height_px;
   cudaStream_t st = dev.stream;
   rbk::KScene k = base;
+  po.pair = k.pair != 0;
   if (image_target) RB_CUDA(ctx, join_default_stream(dev));
   RB_CUDA(ctx, dev.sources.ensure(sizeof(double) * 3 * n));
   RB_CUDA(ctx, cudaMemcpyAsync(dev.sources.p, s->sources, sizeof(double) * 3 * n,
@@ -418,6 +499,10 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   RB_CUDA(ctx, dev.queue.ensure(sizeof(int) * 2));
   RB_CUDA(ctx, cudaMemsetAsync(dev.counters.p, 0, sizeof(unsigned long long) * 8, st));
   RB_CUDA(ctx, cudaMemsetAsync(dev.queue.p, 0, sizeof(int) * 2, st));
+  if (zero_stats) {
+    RB_CUDA(ctx, cudaMemsetAsync(dev.hit.p, 0, sizeof(double) * 2 * n, st));
+    RB_CUDA(ctx, cudaMemsetAsync(dev.landed.p, 0, sizeof(long long) * n, st));
+  }
   k.hit_sum = dev.hit.as<double>();
   k.landed = dev.landed.as<long long>();
   k.counters = dev.counters.as<unsigned long long>();
@@ -426,6 +511,10 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
     RB_CUDA(ctx, dev.landed0.ensure(sizeof(long long) * n));
     RB_CUDA(ctx, dev.counters0.ensure(sizeof(unsigned long long) * 8));
     RB_CUDA(ctx, cudaMemsetAsync(dev.counters0.p, 0, sizeof(unsigned long long) * 8, st));
+    if (zero_stats) {
+      RB_CUDA(ctx, cudaMemsetAsync(dev.hit0.p, 0, sizeof(double) * 2 * n, st));
+      RB_CUDA(ctx, cudaMemsetAsync(dev.landed0.p, 0, sizeof(long long) * n, st));
+    }
     k.hit_sum0 = dev.hit0.as<double>();
     k.landed0 = dev.landed0.as<long long>();
     k.counters0 = dev.counters0.as<unsigned long long>();
@@ -471,6 +560,15 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
     po.launches = 1 + (k.split > 1 && k.n_work > 0 ? 1 : 0);
   }
   RB_CUDA(ctx, cudaEventRecord(dev.ev1, st));
+  return RB_OK;
+}
+
+// Phase 3: per-source stats, counters and the error flag to the host, then
+// wait for the device's stream (which also covers any collective queued on it).
+int collect_on(rb_ctx* ctx, Device& dev, const rb_scene* s, PartialOut& po) {
+  RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
+  const int64_t n = s->n_sources;
+  cudaStream_t st = dev.stream;
   po.hit.assign(2 * n, 0.0);
   po.landed.assign(n, 0);
   if (n) {
@@ -481,7 +579,7 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   }
   RB_CUDA(ctx, cudaMemcpyAsync(po.counters, dev.counters.p, sizeof(unsigned long long) * 6,
                                cudaMemcpyDeviceToHost, st));
-  if (k.pair) {
+  if (po.pair) {
     po.hit0.assign(2 * n, 0.0);
     po.landed0.assign(n, 0);
     if (n) {
@@ -493,10 +591,138 @@ int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
     RB_CUDA(ctx, cudaMemcpyAsync(po.counters0, dev.counters0.p, sizeof(unsigned long long) * 6,
                                  cudaMemcpyDeviceToHost, st));
   }
-  RB_CUDA(ctx, cudaMemcpyAsync(&po.err_flag, k.err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(&po.err_flag, dev.queue.as<int>() + 1, sizeof(int),
+                               cudaMemcpyDeviceToHost, st));
   RB_CUDA(ctx, cudaStreamSynchronize(st));
   RB_CUDA(ctx, cudaEventElapsedTime(&po.ms, dev.ev0, dev.ev1));
   return RB_OK;
+}
+
+// One device renders the given work list (rb_trace_shard): phase 1 + phase 3.
+int render_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& base,
+              const std::vector<int32_t>& work, unsigned long long* image_target,
+              PartialOut& po) {
+  if (int rc = launch_on(ctx, dev, s, base, work, image_target, false, po)) return rc;
+  return collect_on(ctx, dev, s, po);
+}
+
+// The kernel's error flag (KScene::err_flag) as the reference's exception text.
+int flag_error(rb_ctx* ctx, int flag, const rb_scene* s) {
+  if (flag & 1) return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+  if (flag & 2) {
+    char lim[64];
+    std::snprintf(lim, sizeof lim, "%.6g", std::ldexp(1.0, 22) / std::max(1, s->rays_per_source));
+    return fail(ctx, RB_E_RUNTIME,
+                std::string("rb_trace: a sensor-plane hit (|u| or |v| > ") + lim +
+                    " m) exceeds the fixed-point range of DotHitStats::hit_sum");
+  }
+  return RB_OK;
+}
+
+// Phase 2, the one exchange step, queued on every device's stream after its
+// render.  In-process (one communicator per device): a grouped ncclReduce of
+// the fixed-point images onto device 0; the stats are merged on the host
+// (every source has exactly one owner).  Rank mode (one process per GPU): the
+// same image reduce onto rank 0, plus ncclAllReduce of the per-source stats,
+// the counters and the error flag, so every rank returns the whole call's
+// statistics.  Stats entries have one non-zero contributor and the image is
+// an integer, so every sum is exact: bit-identical for any device count.
+int exchange(rb_ctx* ctx, const rb_scene* s, bool image, bool pair) {
+  NcclApi& api = ctx->nccl;
+  const size_t n = static_cast<size_t>(s->n_sources);
+  const size_t npx = static_cast<size_t>(s->sensor.width_px) * s->sensor.height_px;
+  const bool dist = ctx->world > 1;
+  if (!image && !dist) return RB_OK;
+  if (api.group_start() != ncclSuccess) return fail(ctx, RB_E_CUDA, "ncclGroupStart failed");
+  ncclResult_t r = ncclSuccess;
+  for (size_t d = 0; d < ctx->devs.size() && r == ncclSuccess; ++d) {
+    Device& dv = ctx->devs[d];
+    cudaSetDevice(dv.ordinal);
+    ncclComm_t c = ctx->comms[d];
+    cudaStream_t st = dv.stream;
+    if (image) r = api.reduce(dv.image.p, dv.image.p, npx, ncclUint64, ncclSum, 0, c, st);
+    if (dist && r == ncclSuccess) {
+      ncclResult_t q[8] = {
+          api.all_reduce(dv.hit.p, dv.hit.p, 2 * n, ncclFloat64, ncclSum, c, st),
+          api.all_reduce(dv.landed.p, dv.landed.p, n, ncclInt64, ncclSum, c, st),
+          api.all_reduce(dv.counters.p, dv.counters.p, 8, ncclUint64, ncclSum, c, st),
+          api.all_reduce(dv.queue.as<int>() + 1, dv.queue.as<int>() + 1, 1, ncclInt32, ncclMax,
+                         c, st),
+          ncclSuccess, ncclSuccess, ncclSuccess, ncclSuccess};
+      if (pair) {
+        q[4] = api.all_reduce(dv.hit0.p, dv.hit0.p, 2 * n, ncclFloat64, ncclSum, c, st);
+        q[5] = api.all_reduce(dv.landed0.p, dv.landed0.p, n, ncclInt64, ncclSum, c, st);
+        q[6] = api.all_reduce(dv.counters0.p, dv.counters0.p, 8, ncclUint64, ncclSum, c, st);
+      }
+      for (ncclResult_t x : q)
+        if (x != ncclSuccess) r = x;
+    }
+  }
+  const ncclResult_t e = api.group_end();
+  if (r != ncclSuccess || e != ncclSuccess)
+    return fail(ctx, RB_E_CUDA,
+                "NCCL collective failed (NCCL error " + std::to_string(r != ncclSuccess ? r : e) +
+                    ")");
+  return RB_OK;
+}
+
+// Renders this process's shards — device d of rank r takes shard r * nd + d
+// of world * nd, from the same Z-order plan as rb_plan_shards — and combines
+// them (exchange).  Every device takes part even when its shard is empty, so
+// the collectives always see every rank.
+int run_shards(rb_ctx* ctx, const rb_scene* s, const rbk::KScene& base,
+               std::vector<std::vector<int32_t>>& work, std::vector<PartialOut>& parts) {
+  const int nd = static_cast<int>(ctx->devs.size());
+  const int64_t total = static_cast<int64_t>(nd) * ctx->world;
+  const std::vector<int32_t> z = zorder(s);
+  work.assign(nd, {});
+  for (int d = 0; d < nd; ++d) work[d] = shard_list(z, static_cast<int64_t>(ctx->rank) * nd + d, total);
+  parts.assign(nd, PartialOut{});
+  const bool dist = ctx->world > 1;
+  if (int rc = for_each_device(ctx, [&](Device& dev) -> int {
+        const size_t i = static_cast<size_t>(&dev - ctx->devs.data());
+        return launch_on(ctx, dev, s, base, work[i], nullptr, dist, parts[i]);
+      }))
+    return rc;
+  if (total > 1)
+    if (int rc = exchange(ctx, s, base.accumulate != 0, base.pair != 0)) return rc;
+  if (int rc = for_each_device(ctx, [&](Device& dev) -> int {
+        const size_t i = static_cast<size_t>(&dev - ctx->devs.data());
+        return collect_on(ctx, dev, s, parts[i]);
+      }))
+    return rc;
+  for (const PartialOut& po : parts)
+    if (po.err_flag) return flag_error(ctx, po.err_flag, s);
+  return RB_OK;
+}
+
+// Per-source DotHitStats and counters of one leg out of run_shards' parts.
+void merge_stats(const rb_ctx* ctx, const rb_scene* s,
+                 const std::vector<std::vector<int32_t>>& work,
+                 const std::vector<PartialOut>& parts, bool leg0, double* hit_sum, int64_t* landed,
+                 unsigned long long c[6], int64_t& landed_total) {
+  landed_total = 0;
+  for (int j = 0; j < 6; ++j) c[j] = 0;
+  auto take = [&](const PartialOut& po, int32_t src) {
+    const std::vector<double>& h = leg0 ? po.hit0 : po.hit;
+    const std::vector<long long>& l = leg0 ? po.landed0 : po.landed;
+    if (hit_sum) {
+      hit_sum[2 * src] = h[2 * src];
+      hit_sum[2 * src + 1] = h[2 * src + 1];
+    }
+    if (landed) landed[src] = l[src];
+    landed_total += l[src];
+  };
+  if (ctx->world > 1) {  // all-reduced: device 0 holds every source and the totals
+    const PartialOut& po = parts[0];
+    for (int32_t src = 0; src < static_cast<int32_t>(s->n_sources); ++src) take(po, src);
+    for (int j = 0; j < 6; ++j) c[j] = leg0 ? po.counters0[j] : po.counters[j];
+    return;
+  }
+  for (size_t d = 0; d < parts.size(); ++d) {
+    for (int j = 0; j < 6; ++j) c[j] += leg0 ? parts[d].counters0[j] : parts[d].counters[j];
+    for (int32_t src : work[d]) take(parts[d], src);
+  }
 }
 
 void fill_report(rb_trace_out* out, const rb_scene* s, int64_t owned_sources,
@@ -598,6 +824,16 @@ int check_field_desc(rb_ctx* ctx, const rb_field_desc* d) {
   return RB_OK;
 }
 
+// A failed field load leaves no field behind (and no device memory held).
+int drop_field(rb_ctx* ctx, int rc) {
+  for (Device& dev : ctx->devs) {
+    free_field(dev);
+    for (Buf& b : dev.f64) b.release();
+  }
+  ctx->has_field = ctx->has_field64 = false;
+  return rc;
+}
+
 void set_box(rb_ctx* ctx, const rb_field_desc* d) {
   ctx->field = *d;
   // GriddedField::bounds, scene.cpp:94-97
@@ -619,6 +855,109 @@ const char* rb_last_error(const rb_ctx* ctx) { return ctx ? ctx->last_error.c_st
 
 int rb_device_count(const rb_ctx* ctx) { return ctx ? static_cast<int>(ctx->devs.size()) : 0; }
 
+}  // extern "C"
+
+namespace {
+
+void destroy_device(Device& d) {
+  free_field(d);
+  for (Buf& b : d.f64) b.release();
+  for (Buf* b : {&d.qimage, &d.dbg, &d.dbg_n, &d.hit0, &d.landed0, &d.counters0, &d.hit_part,
+                 &d.landed_part, &d.hit_part0, &d.landed_part0, &d.sources, &d.ids, &d.order,
+                 &d.image, &d.hit, &d.landed, &d.counters, &d.queue, &d.err, &d.dimage,
+                 &d.rays_src, &d.rays_idx, &d.rays_uv, &d.rays_status, &d.rays_steps})
+    b->release();
+  if (d.ev0) cudaEventDestroy(d.ev0);
+  if (d.ev1) cudaEventDestroy(d.ev1);
+  if (d.ev_join) cudaEventDestroy(d.ev_join);
+  if (d.stream) cudaStreamDestroy(d.stream);
+  d.ev0 = d.ev1 = d.ev_join = nullptr;
+  d.stream = nullptr;
+}
+
+void destroy_ctx(rb_ctx* ctx) {
+  for (ncclComm_t c : ctx->comms)
+    if (c && ctx->nccl.destroy) ctx->nccl.destroy(c);
+  ctx->comms.clear();
+  for (Device& d : ctx->devs) destroy_device(d);
+  delete ctx;
+}
+
+// A context over the given device ordinals (streams, events, occupancy).
+int make_ctx(const int* ordinals, int n, rb_ctx** out, char* err, size_t errlen) {
+  if (!out) return fail(nullptr, RB_E_INVALID, "rb_create: out is NULL", err, errlen);
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(nullptr, RB_E_NODEVICE,
+                std::string("rb_create: no CUDA device (") + cudaGetErrorString(e) +
+                    "); this library has no CPU fallback",
+                err, errlen);
+  if (n < 1) return fail(nullptr, RB_E_INVALID, "rb_create: no devices requested", err, errlen);
+  for (int i = 0; i < n; ++i)
+    if (ordinals[i] < 0 || ordinals[i] >= count)
+      return fail(nullptr, RB_E_INVALID, "rb_create: device ordinal out of range", err, errlen);
+  auto* ctx = new rb_ctx();
+  for (int i = 0; i < n; ++i) {
+    Device dev;
+    dev.ordinal = ordinals[i];
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, dev.ordinal);
+    if (prop.major != 10) {
+      destroy_ctx(ctx);
+      return fail(nullptr, RB_E_NODEVICE,
+                  std::string("rb_create: device ") + prop.name +
+                      " is not sm_100 (Blackwell B200); this build targets sm_100a only",
+                  err, errlen);
+    }
+    cudaSetDevice(dev.ordinal);
+    dev.sms = prop.multiProcessorCount;
+    ctx->devs.push_back(std::move(dev));
+    Device& d = ctx->devs.back();
+    if (cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&d.ev0) != cudaSuccess || cudaEventCreate(&d.ev1) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      destroy_ctx(ctx);
+      return fail(nullptr, RB_E_CUDA, "rb_create: stream/event creation failed", err, errlen);
+    }
+    rbk::render_occupancy(d.blocks_per_sm);
+    for (auto& row : d.blocks_per_sm)
+      for (int& b : row) b = std::max(b, 1);
+  }
+  *out = ctx;
+  return RB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rb_create_devices(const int* devices, int n_devices, rb_ctx** out, char* err, size_t errlen) {
+  if (!devices) return fail(nullptr, RB_E_INVALID, "rb_create: devices is NULL", err, errlen);
+  if (int rc = make_ctx(devices, n_devices, out, err, errlen)) return rc;
+  rb_ctx* ctx = *out;
+  if (n_devices > 1) {  // one communicator per device, all in this process
+    std::string msg;
+    if (!ctx->nccl.load(msg)) {
+      *out = nullptr;
+      destroy_ctx(ctx);
+      return fail(nullptr, RB_E_CUDA, msg, err, errlen);
+    }
+    ctx->comms.assign(n_devices, nullptr);
+    const ncclResult_t r = ctx->nccl.init_all(ctx->comms.data(), n_devices, devices);
+    if (r != ncclSuccess) {
+      ctx->comms.clear();
+      *out = nullptr;
+      destroy_ctx(ctx);
+      return fail(nullptr, RB_E_CUDA,
+                  "rb_create: ncclCommInitAll failed (NCCL error " + std::to_string(r) + ")", err,
+                  errlen);
+    }
+  }
+  return RB_OK;
+}
+
 int rb_create(int n_devices, int first_device, rb_ctx** out, char* err, size_t errlen) {
   if (!out) return fail(nullptr, RB_E_INVALID, "rb_create: out is NULL", err, errlen);
   *out = nullptr;
@@ -634,70 +973,77 @@ int rb_create(int n_devices, int first_device, rb_ctx** out, char* err, size_t e
   const int n = n_devices <= 0 ? count - first_device : n_devices;
   if (first_device + n > count)
     return fail(nullptr, RB_E_INVALID, "rb_create: not enough devices", err, errlen);
-  auto* ctx = new rb_ctx();
-  for (int i = 0; i < n; ++i) {
-    Device dev;
-    dev.ordinal = first_device + i;
-    cudaDeviceProp prop{};
-    cudaGetDeviceProperties(&prop, dev.ordinal);
-    if (prop.major != 10) {
-      delete ctx;
-      return fail(nullptr, RB_E_NODEVICE,
-                  std::string("rb_create: device ") + prop.name +
-                      " is not sm_100 (Blackwell B200); this build targets sm_100a only",
-                  err, errlen);
-    }
-    cudaSetDevice(dev.ordinal);
-    dev.sms = prop.multiProcessorCount;
-    if (cudaStreamCreateWithFlags(&dev.stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreate(&dev.ev0) != cudaSuccess || cudaEventCreate(&dev.ev1) != cudaSuccess ||
-        cudaEventCreateWithFlags(&dev.ev_join, cudaEventDisableTiming) != cudaSuccess) {
-      delete ctx;
-      return fail(nullptr, RB_E_CUDA, "rb_create: stream/event creation failed", err, errlen);
-    }
-    rbk::render_occupancy(dev.blocks_per_sm);
-    for (auto& row : dev.blocks_per_sm)
-      for (int& b : row) b = std::max(b, 1);
-    ctx->devs.push_back(dev);
-  }
-  if (n > 1) {
+  std::vector<int> list(n);
+  for (int i = 0; i < n; ++i) list[i] = first_device + i;
+  return rb_create_devices(list.data(), n, out, err, errlen);
+}
+
+int rb_nccl_unique_id(void* id, size_t len, char* err, size_t errlen) {
+  if (!id || len < sizeof(ncclUniqueId))
+    return fail(nullptr, RB_E_INVALID, "rb_nccl_unique_id: buffer smaller than ncclUniqueId", err,
+                errlen);
+  NcclApi api;
+  std::string msg;
+  if (!api.load(msg)) return fail(nullptr, RB_E_CUDA, msg, err, errlen);
+  ncclUniqueId u;
+  const ncclResult_t r = api.get_unique_id(&u);
+  if (r != ncclSuccess)
+    return fail(nullptr, RB_E_CUDA, "ncclGetUniqueId failed (NCCL error " + std::to_string(r) + ")",
+                err, errlen);
+  std::memcpy(id, &u, sizeof(u));
+  return RB_OK;  // the handle stays open: the communicator will use the same library
+}
+
+int rb_create_rank(int device, int rank, int world, const void* id, size_t len, rb_ctx** out,
+                   char* err, size_t errlen) {
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(nullptr, RB_E_INVALID, "rb_create_rank: bad rank/world", err, errlen);
+  if (world > 1 && (!id || len < sizeof(ncclUniqueId)))
+    return fail(nullptr, RB_E_INVALID, "rb_create_rank: missing ncclUniqueId", err, errlen);
+  if (int rc = make_ctx(&device, 1, out, err, errlen)) return rc;
+  rb_ctx* ctx = *out;
+  ctx->rank = rank;
+  ctx->world = world;
+  if (world > 1) {
     std::string msg;
     if (!ctx->nccl.load(msg)) {
-      delete ctx;
+      *out = nullptr;
+      destroy_ctx(ctx);
       return fail(nullptr, RB_E_CUDA, msg, err, errlen);
     }
-    std::vector<int> list(n);
-    for (int i = 0; i < n; ++i) list[i] = first_device + i;
-    ctx->comms.resize(n);
-    if (ctx->nccl.init_all(ctx->comms.data(), n, list.data()) != ncclSuccess) {
-      delete ctx;
-      return fail(nullptr, RB_E_CUDA, "rb_create: ncclCommInitAll failed", err, errlen);
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    ctx->comms.assign(1, nullptr);
+    cudaSetDevice(device);
+    const ncclResult_t r = ctx->nccl.init_rank(&ctx->comms[0], world, u, rank);
+    if (r != ncclSuccess) {
+      ctx->comms.clear();
+      *out = nullptr;
+      destroy_ctx(ctx);
+      return fail(nullptr, RB_E_CUDA,
+                  "rb_create_rank: ncclCommInitRank failed (NCCL error " + std::to_string(r) + ")",
+                  err, errlen);
     }
   }
-  *out = ctx;
+  return RB_OK;
+}
+
+int rb_comm_info(const rb_ctx* ctx, int* rank, int* world, int* comm_ranks, int* nccl_version) {
+  if (!ctx) return RB_E_INVALID;
+  if (rank) *rank = ctx->rank;
+  if (world) *world = ctx->world;
+  int nr = 1, ver = 0;
+  if (!ctx->comms.empty() && ctx->nccl.count) {
+    ctx->nccl.count(ctx->comms[0], &nr);
+    ctx->nccl.version(&ver);
+  }
+  if (comm_ranks) *comm_ranks = nr;
+  if (nccl_version) *nccl_version = ver;
   return RB_OK;
 }
 
 void rb_destroy(rb_ctx* ctx) {
-  if (!ctx) return;
-  for (ncclComm_t c : ctx->comms)
-    if (c && ctx->nccl.destroy) ctx->nccl.destroy(c);
-  for (Device& d : ctx->devs) {
-    free_field(d);
-    for (Buf& b : d.f64) b.release();
-    for (Buf* b : {&d.qimage, &d.dbg, &d.dbg_n, &d.hit0, &d.landed0, &d.counters0, &d.hit_part,
-                   &d.landed_part, &d.hit_part0, &d.landed_part0})
-      b->release();
-    for (Buf* b : {&d.sources, &d.ids, &d.order, &d.image, &d.hit, &d.landed, &d.counters,
-                   &d.queue, &d.err, &d.dimage, &d.rays_src, &d.rays_idx, &d.rays_uv,
-                   &d.rays_status, &d.rays_steps})
-      b->release();
-    if (d.ev0) cudaEventDestroy(d.ev0);
-    if (d.ev1) cudaEventDestroy(d.ev1);
-    if (d.ev_join) cudaEventDestroy(d.ev_join);
-    if (d.stream) cudaStreamDestroy(d.stream);
-  }
-  delete ctx;
+  if (ctx) destroy_ctx(ctx);
 }
 
 int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, const double* gx,
@@ -705,9 +1051,10 @@ int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, 
   if (!ctx) return RB_E_INVALID;
   if (int rc = check_field_desc(ctx, desc)) return rc;
   if (!n || !gx || !gy || !gz) return fail(ctx, RB_E_INVALID, "rb_set_field_nodes: NULL array");
+  ctx->has_field = ctx->has_field64 = false;
   const size_t count = static_cast<size_t>(desc->nx) * desc->ny * desc->nz;
   const size_t chunk = std::min<size_t>(count, size_t(1) << 24);
-  for (Device& dev : ctx->devs) {
+  const int rc = for_each_device(ctx, [&](Device& dev) -> int {
     if (int rc = upload_grid(ctx, dev, count)) return rc;
     Buf stage;
     RB_CUDA(ctx, stage.ensure(4 * chunk * sizeof(double)));
@@ -732,9 +1079,10 @@ int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, 
       }
     }
     RB_CUDA(ctx, cudaStreamSynchronize(dev.stream));
-    stage.release();
     set_l2_window(dev);
-  }
+    return RB_OK;
+  });
+  if (rc) return drop_field(ctx, rc);
   set_box(ctx, desc);
   return RB_OK;
 }
@@ -779,14 +1127,16 @@ int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rh
   const size_t count = static_cast<size_t>(desc->nx) * desc->ny * desc->nz;
   if (!valid_density(rho, count))
     return fail(ctx, RB_E_INVALID, "DensityVolume: densities must be finite and >= 0");
-  for (Device& dev : ctx->devs) {
+  ctx->has_field = ctx->has_field64 = false;
+  const int rc = for_each_device(ctx, [&](Device& dev) -> int {
     if (int rc = upload_grid(ctx, dev, count)) return rc;
     Buf drho;
     RB_CUDA(ctx, drho.ensure(count * sizeof(float)));
     RB_CUDA(ctx, cudaMemcpyAsync(drho.p, rho, count * sizeof(float), cudaMemcpyHostToDevice,
                                  dev.stream));
-    if (int rc = build_from_device_rho(ctx, dev, desc, drho, gladstone_dale_k)) return rc;
-  }
+    return build_from_device_rho(ctx, dev, desc, drho, gladstone_dale_k);
+  });
+  if (rc) return drop_field(ctx, rc);
   set_box(ctx, desc);
   return RB_OK;
 }
@@ -836,8 +1186,17 @@ int rb_set_field_gvol(rb_ctx* ctx, const char* path, const double* z_center,
   const size_t want = slab_bytes > 0 ? static_cast<size_t>(slab_bytes) : (size_t(64) << 20);
   const size_t planes = std::max<size_t>(1, std::min<size_t>(d.nz, want / (plane * 4)));
   std::vector<Buf> drho(ctx->devs.size());
+  // every early return below releases drho (RAII) and the half-built grids
+  struct DropOnError {
+    rb_ctx* ctx;
+    bool armed = true;
+    ~DropOnError() {
+      if (armed) drop_field(ctx, 0);
+    }
+  } drop_guard{ctx};
   for (size_t i = 0; i < ctx->devs.size(); ++i) {
     if (int rc = upload_grid(ctx, ctx->devs[i], count)) return rc;
+    RB_CUDA(ctx, cudaSetDevice(ctx->devs[i].ordinal));
     RB_CUDA(ctx, drho[i].ensure(count * sizeof(float)));
   }
   float* pinned[2] = {nullptr, nullptr};
@@ -887,8 +1246,12 @@ int rb_set_field_gvol(rb_ctx* ctx, const char* path, const double* z_center,
     used[b] = true;
   }
   if (!valid) return fail(ctx, RB_E_INVALID, "DensityVolume: densities must be finite and >= 0");
-  for (size_t i = 0; i < ctx->devs.size(); ++i)
-    if (int rc = build_from_device_rho(ctx, ctx->devs[i], &d, drho[i], gladstone_dale_k)) return rc;
+  if (int rc = for_each_device(ctx, [&](Device& dev) -> int {
+        const size_t i = static_cast<size_t>(&dev - ctx->devs.data());
+        return build_from_device_rho(ctx, dev, &d, drho[i], gladstone_dale_k);
+      }))
+    return rc;
+  drop_guard.armed = false;
   set_box(ctx, &d);
   if (desc_out) *desc_out = d;
   return RB_OK;
@@ -925,13 +1288,19 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
   }
   const int W = s->sensor.width_px, H = s->sensor.height_px;
   const size_t npx = static_cast<size_t>(W) * H;
-  const int nd = static_cast<int>(ctx->devs.size());
-  out->threads = nd;
+  const int total = static_cast<int>(ctx->devs.size()) * ctx->world;
+  const bool root = ctx->rank == 0;  // the image lands on rank 0, device 0
   out->kernel_ms = 0.0;
   out->kernel_launches = 0;
   if (s->n_sources == 0) {  // engine.cpp:436: one "thread", blank image, no stats
-    if (accumulate_image && out->image) std::memset(out->image, 0, npx * sizeof(double));
-    if (accumulate_image && out->quantized) std::memset(out->quantized, 0, npx * sizeof(uint16_t));
+    if (accumulate_image && root) {
+      if (out->image) std::memset(out->image, 0, npx * sizeof(double));
+      if (out->quantized) std::memset(out->quantized, 0, npx * sizeof(uint16_t));
+      if (out->image_fixed) {
+        RB_CUDA(ctx, cudaSetDevice(ctx->devs[0].ordinal));
+        RB_CUDA(ctx, cudaMemset(out->image_fixed, 0, npx * sizeof(uint64_t)));
+      }
+    }
     const unsigned long long zero[6] = {0, 0, 0, 0, 0, 0};
     fill_report(out, s, 0, zero, 0);
     out->threads = 1;
@@ -939,90 +1308,47 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
     return RB_OK;
   }
   const rbk::KScene base = make_kscene(ctx, s, with_field, accumulate_image);
-  const std::vector<int32_t> z = zorder(s);
-  const int used = static_cast<int>(std::min<int64_t>(nd, (s->n_sources + kShardTile - 1) / kShardTile));
-  std::vector<PartialOut> parts(used);
-  std::vector<int> rcs(used, RB_OK);
-  std::vector<std::vector<int32_t>> work(used);
-  for (int d = 0; d < used; ++d) work[d] = shard_list(z, d, used);
-  if (used == 1) {
-    rcs[0] = render_on(ctx, ctx->devs[0], s, base, work[0], nullptr, parts[0]);
-  } else {
-    std::vector<std::thread> pool;
-    std::mutex mu;
-    for (int d = 0; d < used; ++d)
-      pool.emplace_back([&, d] {
-        const int rc = render_on(ctx, ctx->devs[d], s, base, work[d], nullptr, parts[d]);
-        std::lock_guard<std::mutex> lk(mu);
-        rcs[d] = rc;
-      });
-    for (auto& t : pool) t.join();
-  }
-  for (int d = 0; d < used; ++d)
-    if (rcs[d]) return rcs[d];
-  for (int d = 0; d < used; ++d)
-    if (parts[d].err_flag)
-      return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
-
-  // Combine: stats are owned by exactly one device; counters are integers.
-  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<std::vector<int32_t>> work;
+  std::vector<PartialOut> parts;
+  if (int rc = run_shards(ctx, s, base, work, parts)) return rc;
+  unsigned long long c[6];
   int64_t landed_total = 0;
+  merge_stats(ctx, s, work, parts, false, out->hit_sum, out->landed, c, landed_total);
   float ms = 0.f;
   int launches = 0;
-  for (int d = 0; d < used; ++d) {
-    for (int j = 0; j < 6; ++j) c[j] += parts[d].counters[j];
-    ms = std::max(ms, parts[d].ms);
-    launches += parts[d].launches;
-    for (int32_t src : work[d]) {
-      if (out->hit_sum) {
-        out->hit_sum[2 * src] = parts[d].hit[2 * src];
-        out->hit_sum[2 * src + 1] = parts[d].hit[2 * src + 1];
-      }
-      if (out->landed) out->landed[src] = parts[d].landed[src];
-      landed_total += parts[d].landed[src];
-    }
+  for (const PartialOut& po : parts) {
+    ms = std::max(ms, po.ms);
+    launches += po.launches;
   }
-  if (accumulate_image && out->image) {
+  if (accumulate_image && root && (out->image || out->quantized || out->image_fixed)) {
     Device& d0 = ctx->devs[0];
-    if (used > 1) {  // one NCCL sum of the partial fixed-point images onto device 0
-      if (ctx->nccl.group_start() != ncclSuccess)
-        return fail(ctx, RB_E_CUDA, "ncclGroupStart failed");
-      for (int d = 0; d < used; ++d) {
-        Device& dv = ctx->devs[d];
-        cudaSetDevice(dv.ordinal);
-        if (ctx->nccl.reduce(dv.image.p, dv.image.p, npx, ncclUint64, ncclSum, 0, ctx->comms[d],
-                             dv.stream) != ncclSuccess) {
-          ctx->nccl.group_end();
-          return fail(ctx, RB_E_CUDA, "ncclReduce failed");
-        }
-      }
-      if (ctx->nccl.group_end() != ncclSuccess) return fail(ctx, RB_E_CUDA, "ncclGroupEnd failed");
-      for (int d = 0; d < used; ++d) {
-        cudaSetDevice(ctx->devs[d].ordinal);
-        RB_CUDA(ctx, cudaStreamSynchronize(ctx->devs[d].stream));
-      }
-    }
     RB_CUDA(ctx, cudaSetDevice(d0.ordinal));
-    RB_CUDA(ctx, d0.dimage.ensure(npx * sizeof(double)));
-    RB_CUDA(ctx, rbk::launch_image_finalize(d0.image.as<unsigned long long>(),
-                                            d0.dimage.as<double>(), static_cast<int64_t>(npx),
-                                            d0.stream));
-    ++launches;
-    RB_CUDA(ctx, cudaMemcpyAsync(out->image, d0.dimage.p, npx * sizeof(double),
-                                 cudaMemcpyDeviceToHost, d0.stream));
-    if (out->quantized) {  // render's quantize on device (sensor.cpp:124-135)
-      RB_CUDA(ctx, d0.qimage.ensure(npx * sizeof(uint16_t)));
-      RB_CUDA(ctx, rbk::launch_quantize(d0.dimage.as<double>(), static_cast<int64_t>(npx),
-                                        out->gain, out->bit_depth, d0.qimage.as<uint16_t>(),
-                                        d0.stream));
+    if (out->image_fixed)  // device-resident result: the reduced fixed-point image
+      RB_CUDA(ctx, cudaMemcpyAsync(out->image_fixed, d0.image.p, npx * sizeof(uint64_t),
+                                   cudaMemcpyDeviceToDevice, d0.stream));
+    if (out->image || out->quantized) {
+      RB_CUDA(ctx, d0.dimage.ensure(npx * sizeof(double)));
+      RB_CUDA(ctx, rbk::launch_image_finalize(d0.image.as<unsigned long long>(),
+                                              d0.dimage.as<double>(), static_cast<int64_t>(npx),
+                                              d0.stream));
       ++launches;
-      RB_CUDA(ctx, cudaMemcpyAsync(out->quantized, d0.qimage.p, npx * sizeof(uint16_t),
-                                   cudaMemcpyDeviceToHost, d0.stream));
+      if (out->image)
+        RB_CUDA(ctx, cudaMemcpyAsync(out->image, d0.dimage.p, npx * sizeof(double),
+                                     cudaMemcpyDeviceToHost, d0.stream));
+      if (out->quantized) {  // render's quantize on device (sensor.cpp:124-135)
+        RB_CUDA(ctx, d0.qimage.ensure(npx * sizeof(uint16_t)));
+        RB_CUDA(ctx, rbk::launch_quantize(d0.dimage.as<double>(), static_cast<int64_t>(npx),
+                                          out->gain, out->bit_depth, d0.qimage.as<uint16_t>(),
+                                          d0.stream));
+        ++launches;
+        RB_CUDA(ctx, cudaMemcpyAsync(out->quantized, d0.qimage.p, npx * sizeof(uint16_t),
+                                     cudaMemcpyDeviceToHost, d0.stream));
+      }
     }
     RB_CUDA(ctx, cudaStreamSynchronize(d0.stream));
   }
   fill_report(out, s, s->n_sources, c, landed_total);
-  out->threads = used;
+  out->threads = total;
   out->kernel_ms = ms;
   out->kernel_launches = launches;
   out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1050,7 +1376,7 @@ int rb_trace_shard(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulat
   PartialOut po;
   if (int rc = render_on(ctx, ctx->devs[0], s, base, work, reinterpret_cast<unsigned long long*>(image_fixed), po))
     return rc;
-  if (po.err_flag) return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+  if (po.err_flag) return flag_error(ctx, po.err_flag, s);
   int64_t landed_total = 0;
   for (int32_t src : work) {
     if (out->hit_sum) {
@@ -1143,7 +1469,7 @@ int rb_trace_rays(rb_ctx* ctx, const rb_scene* s, int with_field, int64_t n_rays
   int flag = 0;
   RB_CUDA(ctx, cudaMemcpyAsync(&flag, k.err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   RB_CUDA(ctx, cudaStreamSynchronize(st));
-  if (flag) return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+  if (flag) return flag_error(ctx, flag, s);
   return RB_OK;
 }
 
@@ -1234,7 +1560,7 @@ extern "C" int rb_trace_rays_fp64(rb_ctx* ctx, const rb_scene* s, int with_field
   int flag = 0;
   RB_CUDA(ctx, cudaMemcpyAsync(&flag, k.err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   RB_CUDA(ctx, cudaStreamSynchronize(st));
-  if (flag) return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
+  if (flag) return flag_error(ctx, flag, s);
   return RB_OK;
 }
 
@@ -1337,81 +1663,39 @@ extern "C" int rb_trace_bos_pair(rb_ctx* ctx, const rb_scene* s, rb_trace_out* o
     out_ref->threads = out_grad->threads = 1;
     return RB_OK;
   }
-  const std::vector<int32_t> z = zorder(s);
-  const int nd = static_cast<int>(ctx->devs.size());
-  const int used = static_cast<int>(std::min<int64_t>(nd, (s->n_sources + kShardTile - 1) / kShardTile));
-  std::vector<PartialOut> parts(used);
-  std::vector<std::vector<int32_t>> work(used);
-  for (int d = 0; d < used; ++d) work[d] = shard_list(z, d, used);
-  auto run = [&](const rbk::KScene& base, std::vector<PartialOut>& out) -> int {
-    std::vector<int> rcs(used, RB_OK);
-    if (used == 1) {
-      rcs[0] = render_on(ctx, ctx->devs[0], s, base, work[0], nullptr, out[0]);
-    } else {
-      std::vector<std::thread> pool;
-      for (int d = 0; d < used; ++d)
-        pool.emplace_back([&, d] { rcs[d] = render_on(ctx, ctx->devs[d], s, base, work[d], nullptr, out[d]); });
-      for (auto& t : pool) t.join();
-    }
-    for (int d = 0; d < used; ++d)
-      if (rcs[d]) return rcs[d];
-    for (int d = 0; d < used; ++d)
-      if (out[d].err_flag)
-        return fail(ctx, RB_E_INVALID, "emit_rays: source coincides with aperture point");
-    return RB_OK;
-  };
   // With the cell table the field kernel runs at 3 CTAs/SM and the fused pair
   // kernel (which must also hold the reference leg) at 2: two passes are then
   // faster (bos 1e7 rays: 40.3 ms vs 43.7 ms fused; the no-field pass is <1%).
   // On the node grid both run at 2 CTAs/SM and fusing saves the second raygen.
+  std::vector<std::vector<int32_t>> work;
+  std::vector<PartialOut> parts, ref;
+  unsigned long long c[6], c0[6];
+  int64_t lt = 0, lt0 = 0;
   if (ctx->devs[0].cells) {
-    std::vector<PartialOut> ref(used);
-    if (int rc = run(make_kscene(ctx, s, 0, 0), ref)) return rc;
-    if (int rc = run(make_kscene(ctx, s, 1, 0), parts)) return rc;
-    for (int d = 0; d < used; ++d) {
-      parts[d].hit0.swap(ref[d].hit);
-      parts[d].landed0.swap(ref[d].landed);
-      std::copy(ref[d].counters, ref[d].counters + 6, parts[d].counters0);
-      parts[d].ms += ref[d].ms;
-      parts[d].launches += ref[d].launches;
-    }
+    std::vector<std::vector<int32_t>> work0;
+    if (int rc = run_shards(ctx, s, make_kscene(ctx, s, 0, 0), work0, ref)) return rc;
+    if (int rc = run_shards(ctx, s, make_kscene(ctx, s, 1, 0), work, parts)) return rc;
+    merge_stats(ctx, s, work0, ref, false, out_ref->hit_sum, out_ref->landed, c0, lt0);
+    merge_stats(ctx, s, work, parts, false, out_grad->hit_sum, out_grad->landed, c, lt);
   } else {
     rbk::KScene base = make_kscene(ctx, s, 1, 0);
     base.pair = 1;
-    if (int rc = run(base, parts)) return rc;
+    if (int rc = run_shards(ctx, s, base, work, parts)) return rc;
+    merge_stats(ctx, s, work, parts, true, out_ref->hit_sum, out_ref->landed, c0, lt0);
+    merge_stats(ctx, s, work, parts, false, out_grad->hit_sum, out_grad->landed, c, lt);
   }
-  unsigned long long c[6] = {0, 0, 0, 0, 0, 0}, c0[6] = {0, 0, 0, 0, 0, 0};
-  int64_t lt = 0, lt0 = 0;
   float ms = 0.f;
-  for (int d = 0; d < used; ++d) {
-    for (int j = 0; j < 6; ++j) {
-      c[j] += parts[d].counters[j];
-      c0[j] += parts[d].counters0[j];
-    }
-    ms = std::max(ms, parts[d].ms);
-    for (int32_t src : work[d]) {
-      if (out_grad->hit_sum) {
-        out_grad->hit_sum[2 * src] = parts[d].hit[2 * src];
-        out_grad->hit_sum[2 * src + 1] = parts[d].hit[2 * src + 1];
-      }
-      if (out_grad->landed) out_grad->landed[src] = parts[d].landed[src];
-      if (out_ref->hit_sum) {
-        out_ref->hit_sum[2 * src] = parts[d].hit0[2 * src];
-        out_ref->hit_sum[2 * src + 1] = parts[d].hit0[2 * src + 1];
-      }
-      if (out_ref->landed) out_ref->landed[src] = parts[d].landed0[src];
-      lt += parts[d].landed[src];
-      lt0 += parts[d].landed0[src];
-    }
+  int launches = 0;
+  for (size_t d = 0; d < parts.size(); ++d) {
+    ms = std::max(ms, parts[d].ms + (ref.empty() ? 0.f : ref[d].ms));
+    launches += parts[d].launches + (ref.empty() ? 0 : ref[d].launches);
   }
   c0[5] = 0;  // no RK4 steps on the reference leg
   fill_report(out_grad, s, s->n_sources, c, lt);
   fill_report(out_ref, s, s->n_sources, c0, lt0);
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  out_ref->threads = out_grad->threads = used;
+  out_ref->threads = out_grad->threads = static_cast<int>(ctx->devs.size()) * ctx->world;
   out_ref->kernel_ms = out_grad->kernel_ms = ms;
-  int launches = 0;
-  for (int d = 0; d < used; ++d) launches += parts[d].launches;
   out_ref->kernel_launches = out_grad->kernel_launches = launches;
   out_ref->wall_seconds = out_grad->wall_seconds = wall;
   return RB_OK;

@@ -111,6 +111,7 @@ struct KScene {
   double3 s_center, s_normal, s_eu, s_ev;
   int32_t W, H;
   double pitch, sigma, half_width, inv_s;
+  double hit_limit;                 // |u|, |v| bound keeping a bundle's fixed-point hit sum in int64
   int32_t accumulate, degenerate;   // degenerate: sigma < 1e-3 * pitch
   // outputs
   unsigned long long* image;        // W*H fixed point (radiance * 2^31)

@@ -277,6 +277,17 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
 constexpr double kHitScale = 1099511627776.0;  // 2^40
 __device__ __forceinline__ long long hit_fixed(double u) { return __double2ll_rn(u * kHitScale); }
 __device__ __forceinline__ double hit_double(long long s) { return (double)s * (1.0 / kHitScale); }
+// Adds a landed ray's (u, v) to its thread's fixed-point sums.  The reference
+// does not clip hits to the sensor (sensor.cpp:27-34), so a grazing ray can land
+// arbitrarily far out; past S.hit_limit (2^22 m / rays per emitter) a bundle's
+// sum could wrap int64, and the call reports that (err_flag bit 2) instead of a
+// wrong DotHitStats.
+__device__ __forceinline__ void add_hit(const KScene& S, long long& su, long long& sv, double u,
+                                        double v) {
+  if (fabs(u) > S.hit_limit || fabs(v) > S.hit_limit) atomicOr(S.err_flag, 2);
+  su += hit_fixed(u);
+  sv += hit_fixed(v);
+}
 
 // Deterministic block sum (fixed shuffle tree, fixed warp order).
 template <typename T>
@@ -389,10 +400,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
           if (emit_ray(S, ekey, so, i, d)) {
             const RayResult r0 = finish_ray<kField>(S, so, d, false, sh_rt[tid], &sh_st32[tid]);
             sh_cnt0[r0.status][tid] += 1u;
-            if (r0.status == 0) {
-              sh_uv0[0][tid] += hit_fixed(r0.u);
-              sh_uv0[1][tid] += hit_fixed(r0.v);
-            }
+            if (r0.status == 0) add_hit(S, sh_uv0[0][tid], sh_uv0[1][tid], r0.u, r0.v);
             r = finish_ray<kField>(S, so, d, true, sh_rt[tid], &sh_st32[tid]);
           } else {
             r.status = 1;
@@ -442,8 +450,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
       if (r.status >= 0) {
         sh_cnt[r.status][tid] += 1u;
         if (r.status == 0) {
-          sh_uv[0][tid] += hit_fixed(r.u);
-          sh_uv[1][tid] += hit_fixed(r.v);
+          add_hit(S, sh_uv[0][tid], sh_uv[1][tid], r.u, r.v);
           if (S.accumulate)
             deposit(S, r.u, r.v, tile, vtile[0], vtile[1], vtile[2], vtile[3],
                     (uint32_t)(mix_bits(ekey + (uint64_t)i) >> 32), wsh);

@@ -39,16 +39,57 @@ def plan_shards(scene: FlatScene, shard_count: int) -> np.ndarray:
     return out[: scene.n_sources]
 
 
-class GpuTracer:
-    """Owns an ``rb_ctx``: device streams, the resident density grid, buffers."""
+def nccl_unique_id() -> bytes:
+    """rb_nccl_unique_id: rank 0's communicator id, to hand to every rank."""
+    lib = abi.load_library()
+    buf = C.create_string_buffer(abi.RB_NCCL_UNIQUE_ID_BYTES)
+    err = C.create_string_buffer(1024)
+    rc = lib.rb_nccl_unique_id(buf, abi.RB_NCCL_UNIQUE_ID_BYTES, err, 1024)
+    if rc:
+        raise RaybosError(f"rb_nccl_unique_id failed: {err.value.decode()}")
+    return buf.raw
 
-    def __init__(self, n_devices: int = 1, first_device: int = 0):
+
+class GpuTracer:
+    """Owns an ``rb_ctx``: device streams, the resident density grid, buffers.
+
+    ``GpuTracer(n)`` renders on devices first_device .. first_device+n-1 from
+    this process (``devices=[...]`` names them explicitly);
+    ``GpuTracer.for_rank(device, rank, world, uid)`` is one rank of a
+    one-process-per-GPU job (rb_create_rank)."""
+
+    def __init__(self, n_devices: int = 1, first_device: int = 0, devices=None, _ctx=None):
         self.lib = abi.load_library()
         self.ctx = C.c_void_p()
         err = C.create_string_buffer(1024)
-        rc = self.lib.rb_create(int(n_devices), int(first_device), C.byref(self.ctx), err, 1024)
+        if _ctx is not None:
+            self.ctx = _ctx
+            return
+        if devices is not None:
+            arr = (C.c_int * len(devices))(*[int(d) for d in devices])
+            rc = self.lib.rb_create_devices(arr, len(devices), C.byref(self.ctx), err, 1024)
+        else:
+            rc = self.lib.rb_create(int(n_devices), int(first_device), C.byref(self.ctx), err, 1024)
         if rc:
             raise RaybosError(f"rb_create failed: {err.value.decode()}")
+
+    @classmethod
+    def for_rank(cls, device: int, rank: int, world: int, uid: bytes | None) -> "GpuTracer":
+        lib = abi.load_library()
+        ctx = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        idbuf = C.create_string_buffer(uid, abi.RB_NCCL_UNIQUE_ID_BYTES) if uid else None
+        rc = lib.rb_create_rank(int(device), int(rank), int(world), idbuf,
+                                abi.RB_NCCL_UNIQUE_ID_BYTES if uid else 0, C.byref(ctx), err, 1024)
+        if rc:
+            raise RaybosError(f"rb_create_rank failed: {err.value.decode()}")
+        return cls(_ctx=ctx)
+
+    def comm_info(self) -> dict:
+        """rank / world / ranks of the NCCL communicator / NCCL version (0: stand-in)."""
+        v = [C.c_int() for _ in range(4)]
+        self.lib.rb_comm_info(self.ctx, *[C.byref(x) for x in v])
+        return dict(zip(("rank", "world", "comm_ranks", "nccl_version"), (x.value for x in v)))
 
     def close(self):
         if self.ctx:
@@ -106,21 +147,26 @@ class GpuTracer:
 
     # ---- run_trace -----------------------------------------------------------
     def run_trace(self, scene: FlatScene, with_field: bool = True, accumulate_image: bool = True,
-                  image_out: Optional[np.ndarray] = None, quantize=None) -> TraceResult:
+                  image_out: Optional[np.ndarray] = None, quantize=None,
+                  image_fixed_ptr: int = 0, host_image: bool = True) -> TraceResult:
         """rb_trace.  quantize=(bit_depth, gain) also returns the render tail's
-        quantized uint16 image (computed on device) as result.quantized."""
+        quantized uint16 image (computed on device) as result.quantized.
+        image_fixed_ptr: a device buffer of W*H uint64 that receives the reduced
+        fixed-point image (rb_trace_out.image_fixed); host_image=False then skips
+        the FP64 host image.  In rank mode only rank 0 receives an image."""
         s, keep = scene.to_c()
         n = scene.n_sources
         hit = np.zeros((n, 2))
         landed = np.zeros(n, dtype=np.int64)
         img = None
-        if accumulate_image:
+        if accumulate_image and host_image:
             img = image_out if image_out is not None else np.empty((scene.height, scene.width))
             assert img.dtype == np.float64 and img.flags.c_contiguous and img.size == scene.width * scene.height
         out = abi.TraceOut()
         out.hit_sum = abi.dptr(hit) if n else None
         out.landed = abi.i64ptr(landed) if n else None
         out.image = abi.dptr(img) if img is not None else None
+        out.image_fixed = int(image_fixed_ptr) if image_fixed_ptr else None
         qimg = None
         if quantize is not None and accumulate_image:
             qimg = np.zeros((scene.height, scene.width), dtype=np.uint16)

@@ -95,6 +95,15 @@ def plane_mirror(vertex, axis, diameter) -> abi.Element:
     return e
 
 
+def rotation(axis, degrees) -> np.ndarray:
+    """Right-handed rotation matrix about a unit axis (Rodrigues)."""
+    a = np.asarray(axis, dtype=np.float64)
+    a = a / np.linalg.norm(a)
+    t = math.radians(degrees)
+    K = np.array([[0.0, -a[2], a[1]], [a[2], 0.0, -a[0]], [-a[1], a[0], 0.0]])
+    return np.eye(3) + math.sin(t) * K + (1.0 - math.cos(t)) * (K @ K)
+
+
 def sensor(center, normal, e_u, e_v, width_px, height_px, pitch, window_sigmas=4.0) -> abi.Sensor:
     """raybos::SensorModel (sensor.hpp:19-32) minus bit depth / gain."""
     return abi.Sensor(abi.vec3(center), abi.vec3(normal), abi.vec3(e_u), abi.vec3(e_v),
@@ -215,6 +224,45 @@ class FlatScene:
 
     def dumps(self) -> str:
         return json.dumps(self.to_json())
+
+    def with_camera_moved(self, rot, pivot) -> "FlatScene":
+        """The same scene with the whole camera — pupil, every optical element
+        (centres, axes, surface vertices / axes) and the sensor frame — turned
+        by the rotation matrix ``rot`` about ``pivot``; sources unchanged.  The
+        reference's SceneSetup carries general axes everywhere (optics.hpp:26-36,
+        raygen.hpp:32-36, sensor.hpp:19-32) even though build_scene_setup only
+        builds +z cameras (engine.cpp:258); this is how an off-axis perspective
+        camera is expressed at the run_trace boundary."""
+        R = np.asarray(rot, dtype=np.float64)
+        c = np.asarray(pivot, dtype=np.float64)
+
+        def pt(v):
+            q = R @ (np.array([v.x, v.y, v.z]) - c) + c
+            return abi.vec3(q)
+
+        def ax(v):
+            return abi.vec3(R @ np.array([v.x, v.y, v.z]))
+
+        def surf(x: abi.Surface) -> abi.Surface:
+            return abi.Surface(pt(x.vertex), ax(x.axis), x.curvature_radius, x.aperture_radius,
+                               x.n_before, x.n_after)
+
+        elems = []
+        for e in self.elements:
+            f = abi.Element.from_buffer_copy(e)
+            f.center, f.axis = pt(e.center), ax(e.axis)
+            f.front, f.back = surf(e.front), surf(e.back)
+            elems.append(f)
+        se = self.sensor
+        out = FlatScene(**{k: getattr(self, k) for k in self.__dataclass_fields__})
+        pc = pt(abi.vec3(self.pupil_center))
+        pa = ax(abi.vec3(self.pupil_axis))
+        out.pupil_center = (pc.x, pc.y, pc.z)
+        out.pupil_axis = (pa.x, pa.y, pa.z)
+        out.elements = elems
+        out.sensor = abi.Sensor(pt(se.center), ax(se.normal), ax(se.e_u), ax(se.e_v), se.width_px,
+                                se.height_px, se.pitch, se.window_sigmas)
+        return out
 
     def subset(self, idx) -> "FlatScene":
         """The same scene restricted to sources idx, keeping their RNG streams."""

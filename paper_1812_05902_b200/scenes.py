@@ -10,8 +10,10 @@ are synthetic and seeded; nothing is downloaded.
   bos     20,480 dots x 1e4 rays through a 256^3 BDT-like field (64 mm cube), 1024^2
   tomo    1e5 particles x 1e4 rays (1e9) inside a 256x256x128 normal-shock field,
           thick singlet camera, 2048^2                                  <- headline
-  optics  1e4 particles x 1e4 rays, f/2.8 singlet, +-20 mm depth, off-axis box, 1024^2
-  large   4e5 dots x 1e4 rays through a 1024^3 grid (16 GiB float4), 4096^2
+  optics  1e4 particles x 1e4 rays, f/2.8 singlet, +-20 mm depth, off-axis perspective
+          camera (turned 20 deg / 6 deg about the box centre), 1024^2
+  large   4e5 dots x 1e4 rays through a 1024^3 grid (16 GiB float4), 4096^2, fine
+          step (h = spacing / 4, half the reference default)
 """
 from __future__ import annotations
 
@@ -135,15 +137,26 @@ def config(name: str, scale: float = 1.0):
         cfg = _cfg({"type": "particles", "count": n_src, "diameter_m": 5e-6, "seed": 13,
                     "box_lo_m": [-0.01, -0.03, -0.02], "box_hi_m": [0.03, 0.03, 0.02]},
                    (1024, 1024), 10000, SINGLET_F28, seed=6)
-        return cfg, None, {"emitters": n_src}
+        return cfg, None, {"emitters": n_src, "camera": OPTICS_CAMERA}
     if name == "large":
         ext = 4096 * 1e-5 / 0.12
         n_src = int(400000 * scale)
+        # BASELINE's "fine integration step": half the reference default
+        # (engine.cpp:244-252 takes h = spacing / 2), i.e. h = spacing / 4
+        h = 0.25 * 0.256 / 1023
         cfg = _cfg({"type": "dots", "extent_m": [ext, ext], "count": n_src, "seed": 17},
-                   (4096, 4096), 10000, THIN, magnification=0.12)
+                   (4096, 4096), 10000, THIN, magnification=0.12, delta_xi=h)
         grid = bdt_field(1024, 1024, 0.256, 0.256, amplitude=0.1)
-        return cfg, grid, {"field": "1024^3 BDT-like, 256 mm cube"}
+        return cfg, grid, {"field": "1024^3 BDT-like, 256 mm cube, fine step h = spacing/4"}
     raise ValueError(f"unknown scene '{name}'")
+
+
+# The optics scene's off-axis perspective camera (BASELINE configs[3]): the
+# whole +z camera build_scene_setup makes (pupil, f/2.8 singlet, sensor frame)
+# turned 20 deg about y and 6 deg about x around the particle box's centre, so
+# the box is seen obliquely (perspective foreshortening, depth-varying defocus)
+# and every optical axis is general.
+OPTICS_CAMERA = {"pivot": (0.01, 0.0, 0.0), "rot_y_deg": 20.0, "rot_x_deg": 6.0}
 
 
 def build(name: str, calibrate=None, scale: float = 1.0):
@@ -156,4 +169,13 @@ def build(name: str, calibrate=None, scale: float = 1.0):
     if calibrate is None:
         c.sensor["gain"] = 1.0
     scene, field, info = S.build_scene(c, calibrate=calibrate)
+    cam = desc.get("camera")
+    if cam:  # SceneSetup-level camera move (the gain was calibrated on the +z camera)
+        from .scene import rotation
+        rot = rotation((1.0, 0.0, 0.0), cam["rot_x_deg"]) @ rotation((0.0, 1.0, 0.0),
+                                                                     cam["rot_y_deg"])
+        scene = scene.with_camera_moved(rot, cam["pivot"])
+        desc = dict(desc, camera=f"off-axis perspective: camera turned {cam['rot_y_deg']} deg "
+                                 f"about y, {cam['rot_x_deg']} deg about x around "
+                                 f"{cam['pivot']}")
     return scene, field, info, desc

@@ -5,6 +5,9 @@
 // gathers, so bench.py measures those two roofs on the box:
 //   * FP32 FFMA throughput (register-operand and immediate-operand forms)
 //   * L2-resident float4 gather bandwidth (LDG.128 over a 64 MiB working set)
+//   * shared-memory RED.ADD.U32 throughput (the sensor deposition's per-pixel
+//     operation: the binding roof of the scenes without a medium)
+//   * FP64 DFMA throughput (raygen / optics / sensor stages)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -61,9 +64,98 @@ __global__ void __launch_bounds__(256) gather_kernel(const float4* __restrict__ 
   if (acc == 12345.678f) out[0] = acc;
 }
 
+// Shared-memory RED.ADD.U32 throughput (the deposition's per-pixel operation,
+// render.cuh red_shared): each thread adds to its own words, bank-conflict free.
+__global__ void __launch_bounds__(256) red_shared_kernel(float* out, int iters) {
+  __shared__ unsigned tile[256 * 8];
+  for (int j = 0; j < 8; ++j) tile[j * 256 + threadIdx.x] = 0u;
+  __syncthreads();
+  const unsigned base = (unsigned)__cvta_generic_to_shared(tile) + 4u * threadIdx.x;
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base + 1024u * j), "r"(i + j) : "memory");
+  __syncthreads();
+  unsigned s = 0;
+  for (int j = 0; j < 8; ++j) s += tile[j * 256 + threadIdx.x];
+  if (s == 0x12345u) out[threadIdx.x] = (float)s;
+}
+
+// FP64 DFMA throughput (the FP64 raygen / optics / sensor stages).
+__global__ void __launch_bounds__(256) dfma_kernel(double* out, double b, double c, int iters) {
+  double a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * 1e-3 + j;
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = fma(a[j], b, c);
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 }  // namespace
 
 extern "C" {
+
+// Best-of-5 shared-memory RED.ADD.U32 throughput in Gop/s.
+double rbp_red_shared_gops(int device) {
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float* out = nullptr;
+  cudaMalloc(&out, 1024 * sizeof(float));
+  const int blocks = sms * 8, threads = 256, iters = 1 << 12;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(e0);
+    red_shared_kernel<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = 8.0 * iters * (double)blocks * threads;
+    if (rep > 0) best = std::max(best, ops / (ms * 1e-3) / 1e9);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? best : -1.0;
+}
+
+// Best-of-5 FP64 DFMA throughput in TFLOP/s (2 flops per FMA).
+double rbp_dfma_tflops(int device) {
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* out = nullptr;
+  cudaMalloc(&out, 1024 * sizeof(double));
+  const int blocks = sms * 8, threads = 256, iters = 1 << 12;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(e0);
+    dfma_kernel<<<blocks, threads>>>(out, 0.999, 1e-3, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 8.0 * iters * (double)blocks * threads;
+    if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? best : -1.0;
+}
 
 // Best-of-5 FP32 FFMA throughput in TFLOP/s (2 flops per FMA).  mode 0:
 // register operands, 1: immediate operands, 2: packed pairs (FFMA2).

@@ -94,6 +94,23 @@ FIXTURES = {
                                       "box_hi_m": [0.005, 0.005, 0.253]},
                                      {"type": "none"}, sensor=(128, 128), rays=800, seed=12),
                             density="shock"),
+    # folded camera: aperture + thin lens + a 45-degree plane mirror (reflect_on_mirror,
+    # optics.cpp:134-141) turning the beam to +y onto a sensor facing -y, through
+    # the Gaussian blob field
+    "mirror_fold": dict(json=cfg({"type": "dots", "extent_m": [0.012, 0.012], "count": 20,
+                                  "seed": 23}, BLOB, sensor=(160, 160), rays=600, seed=41),
+                        camera="fold"),
+    # off-axis perspective camera: the whole camera (pupil, thick singlet, sensor
+    # frame) turned 14 deg about y and -9 deg about x around the centre of a
+    # normal-shock volume, so plane_basis, the singlet's spherical caps and the
+    # sensor basis all run with general axes (SceneSetup level, as build_scene_setup
+    # only builds +z cameras, engine.cpp:258)
+    "tilted_camera": dict(json=cfg({"type": "particles", "count": 24, "diameter_m": 5e-6,
+                                    "seed": 29, "box_lo_m": [-0.005, -0.005, 0.247],
+                                    "box_hi_m": [0.005, 0.005, 0.253]},
+                                   {"type": "none"}, optics=SINGLET, sensor=(160, 160),
+                                   rays=700, sampling="uniform-random", seed=37),
+                          density="shock", camera="tilt"),
     # single-ray bundles (raygen.cpp:45-46) and the 15.03 um spot convention
     "single_ray": dict(json=cfg({"type": "dots", "extent_m": [0.01, 0.01], "count": 50,
                                  "seed": 2}, SLAB, sensor=(96, 96), rays=1, seed=8,
@@ -126,12 +143,42 @@ def density(kind):
     return g, h, int(4.0 * np.linalg.norm(hi - lo) / h) + 64
 
 
+def move_camera(scene, kind):
+    """SceneSetup-level cameras the reference's config schema cannot express."""
+    from paper_1812_05902_b200 import abi
+    from paper_1812_05902_b200.scene import plane_mirror, rotation
+    if kind == "tilt":
+        rot = rotation((1.0, 0.0, 0.0), -9.0) @ rotation((0.0, 1.0, 0.0), 14.0)
+        return scene.with_camera_moved(rot, (0.0, 0.0, 0.25))
+    # fold: mirror 40 mm behind the lens, normal (0, 1, -1)/sqrt(2); everything the
+    # beam meets after it (the sensor) is reflected through the mirror plane
+    lens_z = max(e.center.z for e in scene.elements)
+    m = np.array([0.0, 0.0, lens_z + 0.04])
+    n = np.array([0.0, 1.0, -1.0]) / np.sqrt(2.0)
+    H = np.eye(3) - 2.0 * np.outer(n, n)
+
+    def refl_pt(v):
+        return abi.vec3(H @ (np.array([v.x, v.y, v.z]) - m) + m)
+
+    def refl_ax(v):
+        return abi.vec3(H @ np.array([v.x, v.y, v.z]))
+
+    se = scene.sensor
+    scene.elements = list(scene.elements) + [plane_mirror(m, n, 0.06)]
+    scene.sensor = abi.Sensor(refl_pt(se.center), refl_ax(se.normal), refl_ax(se.e_u),
+                              refl_ax(se.e_v), se.width_px, se.height_px, se.pitch,
+                              se.window_sigmas)
+    return scene
+
+
 def make(name, spec, n_ray_samples=2048):
     ref = Reference(json_text=spec.get("json"), builtin=spec.get("builtin"))
     if spec.get("density"):
         grid, h, max_steps = density(spec["density"])
         ref.set_field_density(grid)
         ref.lib().refshim_set_step(ref.h, h, max_steps)
+    if spec.get("camera"):
+        ref.set_flat(move_camera(ref.scene(), spec["camera"]))
     scene = ref.scene()
     if spec.get("density"):
         out_rho = {"field_rho": grid.rho, "field_k": np.array(grid.gladstone_dale)}

@@ -59,7 +59,7 @@ def test_ctypes_layout_matches_c(tmp_path):
         "rb_trace_out": ["hit_sum", "landed", "image", "emitted", "landed_total", "lost",
                          "blocked_aperture", "blocked_miss", "blocked_tir", "blocked_sensor_miss",
                          "wall_seconds", "threads", "config_hash", "total_steps", "kernel_ms",
-                         "quantized", "gain", "bit_depth", "kernel_launches"],
+                         "quantized", "gain", "bit_depth", "kernel_launches", "image_fixed"],
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "raybos_gpu.h"', 'int main(void){']
     for st, fs in fields.items():
