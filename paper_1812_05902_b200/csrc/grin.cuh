@@ -20,6 +20,12 @@
 #ifndef RB_UNIFORM_RELOAD
 #define RB_UNIFORM_RELOAD 0  // see sample_d_poly
 #endif
+#ifndef RB_NPLUS1
+#define RB_NPLUS1 1  // see cell_coefficients (measured +2.0% tomo, +1.8% bos)
+#endif
+#ifndef RB_BFROMQ
+#define RB_BFROMQ 1  // see the stage-b point in grin_trace (+0.5% more)
+#endif
 
 
 // Grid geometry, read straight from the kernel parameters (constant bank) so
@@ -57,7 +63,10 @@ __device__ __forceinline__ void cell_coefficients(float4 c000, float4 c100, floa
                                                   float4 c011, float4 c111, float4& a, float4& b,
                                                   float4& c, float4& d, float4& e, float4& f,
                                                   float4& g, float4& h) {
-  a = c000;
+  // RB_NPLUS1: the constant term of the n channel carries the +1, so a sample
+  // yields n itself (one FADD less per sample; n is only a factor of D = n grad n,
+  // so its FP32 rounding at magnitude 1 is a 6e-8 relative error of D)
+  a = RB_NPLUS1 ? make_float4(c000.x + 1.0f, c000.y, c000.z, c000.w) : c000;
   b = f4sub(c100, c000);
   c = f4sub(c010, c000);
   d = f4sub(c001, c000);
@@ -149,14 +158,14 @@ __device__ __forceinline__ float3 poly_eval(const CellPoly& P, float fx, float f
   const float2 xy = f2up(RB_HORNER2(x, y));
   const unsigned long long zw = RB_HORNER2(z, w);
 #undef RB_HORNER2
-  const float n = 1.0f + xy.x;
+  const float n = RB_NPLUS1 ? xy.x : 1.0f + xy.x;
   const float2 nzw = f2up(fmul2(n, zw));
   return make_float3(xy.y * n, nzw.x, nzw.y);
 #else
 #define RB_HORNER(ch)                                                                         \
   fmaf(fx, fmaf(fz, P.f.ch, fmaf(fy, fmaf(fz, P.h.ch, P.e.ch), P.b.ch)),                     \
        fmaf(fy, fmaf(fz, P.g.ch, P.c.ch), fmaf(fz, P.d.ch, P.a.ch)))
-  const float n = 1.0f + RB_HORNER(x);
+  const float n = RB_NPLUS1 ? RB_HORNER(x) : 1.0f + RB_HORNER(x);
   return make_float3(RB_HORNER(y) * n, RB_HORNER(z) * n, RB_HORNER(w) * n);
 #undef RB_HORNER
 #endif
@@ -284,14 +293,24 @@ __device__ __forceinline__ int grin_trace(const KScene& S, double3& o, double3& 
 #pragma unroll kStepUnroll
   for (; step < max_steps; ++step) {
     const float fs = (float)step;
+#if RB_BFROMQ
+    // stage-b base r_i + T0 h/2 taken from the stage-a point (q_a = anchor_i +
+    // dr_i) instead of anchor_{i+1/2} + dr_i: one FFMA instead of FFMA + FADD
+    // per axis; the anchor of the accepted point (pc below) is still
+    // re-evaluated from the step index, so nothing accumulates
+    const float pbx = fmaf(ax, 0.5f, qax), pby = fmaf(ay, 0.5f, qay), pbz = fmaf(az, 0.5f, qaz);
+    const float pdx = 0.f, pdy = 0.f, pdz = 0.f;
+#else
     const float pbx = fmaf(ax, fs + 0.5f, q0x), pby = fmaf(ay, fs + 0.5f, q0y),
                 pbz = fmaf(az, fs + 0.5f, q0z);
+    const float pdx = drx, pdy = dry, pdz = drz;
+#endif
     const float pcx = fmaf(ax, fs + 1.0f, q0x), pcy = fmaf(ay, fs + 1.0f, q0y),
                 pcz = fmaf(az, fs + 1.0f, q0z);
     const float3 Da = RB_SAMPLE_D(qax, qay, qaz);
-    const float3 Db = RB_SAMPLE_D(fmaf(Da.x, S.kbx, fmaf(dtx, S.hhx, pbx + drx)),
-                               fmaf(Da.y, S.kby, fmaf(dty, S.hhy, pby + dry)),
-                               fmaf(Da.z, S.kbz, fmaf(dtz, S.hhz, pbz + drz)));
+    const float3 Db = RB_SAMPLE_D(fmaf(Da.x, S.kbx, fmaf(dtx, S.hhx, RB_BFROMQ ? pbx : pbx + pdx)),
+                               fmaf(Da.y, S.kby, fmaf(dty, S.hhy, RB_BFROMQ ? pby : pby + pdy)),
+                               fmaf(Da.z, S.kbz, fmaf(dtz, S.hhz, RB_BFROMQ ? pbz : pbz + pdz)));
     const float bx = fmaf(dtx, S.hx, drx), by = fmaf(dty, S.hy, dry), bz = fmaf(dtz, S.hz, drz);
     const float3 Dc = RB_SAMPLE_D(fmaf(Db.x, S.kcx, pcx + bx), fmaf(Db.y, S.kcy, pcy + by),
                                fmaf(Db.z, S.kcz, pcz + bz));

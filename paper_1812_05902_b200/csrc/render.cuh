@@ -297,6 +297,63 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+#ifndef RB_STRAIGHT_PILOT
+#define RB_STRAIGHT_PILOT 1
+#endif
+
+// Ray index of this lane in patch slot `slot` (k * warps + warp) of the strided
+// patch order, or -1 past the lattice (kernels.h KScene::band_rays).
+__device__ __forceinline__ int patch_ray(const KScene& S, int slot, int lane, int N) {
+  if (slot >= S.patch_count) return -1;
+  const int p = (int)(((long long)slot * S.patch_stride) % S.patch_count);
+  const int j = p * 32 + lane;  // position in the 4-row bands (kernels.h)
+  const int band = j / S.band_rays, rem = j - band * S.band_rays;
+  const int cx = rem >> 2, cy = band * 4 + (rem & 3);
+  return cy * S.cells + cx < N ? cy * S.cells + cx : -1;
+}
+
+// Grows the unit's pilot bounding box by a landed ray's spot_pixel_window
+// (sensor.cpp:44-55), clipped to the frame.
+__device__ __forceinline__ void pilot_box(const KScene& S, double u, double v, int* sh_box) {
+  const double cc = u / S.pitch + 0.5 * S.W;
+  const double rc = 0.5 * S.H - v / S.pitch;
+  const int c0 = max((int)floor(cc - S.half_width), 0);
+  const int c1 = min((int)floor(cc + S.half_width), S.W - 1);
+  const int r0 = max((int)floor(rc - S.half_width), 0);
+  const int r1 = min((int)floor(rc + S.half_width), S.H - 1);
+  if (c0 <= c1 && r0 <= r1) {
+    atomicMin(&sh_box[0], c0);
+    atomicMin(&sh_box[1], r0);
+    atomicMax(&sh_box[2], c1);
+    atomicMax(&sh_box[3], r1);
+  }
+}
+
+// Places the unit's shared tile over the pilot box (+2 px margin, at most
+// kTileCap words) and zeroes it.  Called by the whole CTA.
+__device__ __forceinline__ void place_tile(const KScene& S, int tid, int* sh_box, int* sh_tile,
+                                           uint32_t* tile) {
+  __syncthreads();
+  if (tid == 0 && sh_box[2] >= 0) {
+    const int m = 2;
+    const int bw = sh_box[2] - sh_box[0] + 1 + 2 * m, bh = sh_box[3] - sh_box[1] + 1 + 2 * m;
+    int tw = min(bw, S.W), th = min(bh, S.H);
+    if (tw * th > kTileCap) {
+      const float f = sqrtf((float)kTileCap / (float)(tw * th));
+      tw = max(1, min(tw, (int)(tw * f)));
+      th = max(1, min(th, kTileCap / tw));
+    }
+    const int ccen = (sh_box[0] + sh_box[2]) / 2, rcen = (sh_box[1] + sh_box[3]) / 2;
+    sh_tile[0] = min(max(ccen - tw / 2, 0), S.W - tw);
+    sh_tile[1] = min(max(rcen - th / 2, 0), S.H - th);
+    sh_tile[2] = tw;
+    sh_tile[3] = th;
+  }
+  __syncthreads();
+  for (int q = tid; q < sh_tile[2] * sh_tile[3]; q += kBlock) tile[q] = 0u;
+  __syncthreads();
+}
+
 // ------------------------------------------------ K1: render_emitters
 // Persistent CTAs pull work units from a queue: a unit is one chunk (KScene::
 // split) of one emitter's bundle, i.e. a range of patch iterations, each of
@@ -380,16 +437,29 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
     // (Taking the patches after the pilot from a shared counter instead, so
     // warps with short rays take more, measured no gain: the unit-end barrier
     // waits on the last ray's length, not on the patch count.)
-    for (int k = kb; k < ke; ++k) {
-      int i = -1;
-      const int slot = k * kWarps + warp;
-      if (slot < S.patch_count) {
-        const int p = (int)(((long long)slot * S.patch_stride) % S.patch_count);
-        const int j = p * 32 + lane;  // position in the 4-row bands (kernels.h)
-        const int band = j / S.band_rays, rem = j - band * S.band_rays;
-        const int cx = rem >> 2, cy = band * 4 + (rem & 3);
-        if (cy * S.cells + cx < N) i = cy * S.cells + cx;
+    // Straight pilot (field kernels): the unit's shared tile is placed from the
+    // first patch iteration's rays traced WITHOUT the medium (raygen + optics +
+    // sensor, ~1% of a ray through the field), so the CTA synchronises right
+    // after the unit starts instead of after its slowest warp's first ray has
+    // crossed the volume (BOS: 2 patch iterations per unit, ~10% of warp time
+    // was spent waiting at that barrier).  The medium only shifts spots by the
+    // deflection (~1 px, inside the tile margin); a spot that leaves the tile
+    // anyway is added to the global image directly, so the image is the same.
+    constexpr bool kStraightPilot = RB_STRAIGHT_PILOT && kField != 0;
+    if (kStraightPilot && S.accumulate) {
+      const int i = patch_ray(S, kb * kWarps + warp, lane, N);
+      if (i >= 0) {
+        const double3 so = make_double3(vso[0], vso[1], vso[2]);
+        double3 d;
+        if (emit_ray(S, *vkey, so, i, d)) {
+          const RayResult p = finish_ray<kField>(S, so, d, false, sh_rt[tid], &sh_st32[tid]);
+          if (p.status == 0) pilot_box(S, p.u, p.v, sh_box);
+        }
       }
+      place_tile(S, tid, sh_box, sh_tile, tile);
+    }
+    for (int k = kb; k < ke; ++k) {
+      const int i = patch_ray(S, k * kWarps + warp, lane, N);
       const uint64_t ekey = *vkey;
       RayResult r;
       r.status = -1;
@@ -412,40 +482,9 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
         sh_steps[tid] += sh_st32[tid];
         sh_st32[tid] = 0u;
       }
-      if (k == kb && S.accumulate) {  // block-uniform branch
-        if (r.status == 0) {  // spot_pixel_window of the pilot, clipped to the frame
-          const double cc = r.u / S.pitch + 0.5 * S.W;
-          const double rc = 0.5 * S.H - r.v / S.pitch;
-          const int c0 = max((int)floor(cc - S.half_width), 0);
-          const int c1 = min((int)floor(cc + S.half_width), S.W - 1);
-          const int r0 = max((int)floor(rc - S.half_width), 0);
-          const int r1 = min((int)floor(rc + S.half_width), S.H - 1);
-          if (c0 <= c1 && r0 <= r1) {
-            atomicMin(&sh_box[0], c0);
-            atomicMin(&sh_box[1], r0);
-            atomicMax(&sh_box[2], c1);
-            atomicMax(&sh_box[3], r1);
-          }
-        }
-        __syncthreads();
-        if (tid == 0 && sh_box[2] >= 0) {
-          const int m = 2;
-          const int bw = sh_box[2] - sh_box[0] + 1 + 2 * m, bh = sh_box[3] - sh_box[1] + 1 + 2 * m;
-          int tw = min(bw, S.W), th = min(bh, S.H);
-          if (tw * th > kTileCap) {
-            const float f = sqrtf((float)kTileCap / (float)(tw * th));
-            tw = max(1, min(tw, (int)(tw * f)));
-            th = max(1, min(th, kTileCap / tw));
-          }
-          const int ccen = (sh_box[0] + sh_box[2]) / 2, rcen = (sh_box[1] + sh_box[3]) / 2;
-          sh_tile[0] = min(max(ccen - tw / 2, 0), S.W - tw);
-          sh_tile[1] = min(max(rcen - th / 2, 0), S.H - th);
-          sh_tile[2] = tw;
-          sh_tile[3] = th;
-        }
-        __syncthreads();
-        for (int q = tid; q < sh_tile[2] * sh_tile[3]; q += kBlock) tile[q] = 0u;
-        __syncthreads();
+      if (!kStraightPilot && k == kb && S.accumulate) {  // block-uniform branch
+        if (r.status == 0) pilot_box(S, r.u, r.v, sh_box);
+        place_tile(S, tid, sh_box, sh_tile, tile);
       }
       if (r.status >= 0) {
         sh_cnt[r.status][tid] += 1u;

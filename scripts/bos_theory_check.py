@@ -1,0 +1,127 @@
+"""BOS displacement-vs-theory check at the BASELINE BOS shape (configs[1]:
+20,480 dots x 1e4 rays through the 256^3 BDT-like field), reference vs B200.
+
+bos_run (reference engine.cpp:532-603) traces every dot twice (without, then
+with the field), turns the per-dot DotHitStats into displacements
+(measure_dot_displacements, bos.cpp:97-112), grids them (bos.cpp:114-201) and
+compares them with the Eq. 9 theory (theoretical_displacement + compare_fields,
+bos.cpp:203-244): RMS error, peak error, Pearson correlation, node count.
+
+  python scripts/bos_theory_check.py ref  OUT.npz   # build container, CPU, ~1 h on 8 cores
+  python scripts/bos_theory_check.py gpu  REF.npz OUT.json   # GPU box
+
+`ref` runs the UNMODIFIED reference (oracle/_ref) on the scene its own
+build_scene_setup makes from the bench config (the field written as a GVOL file,
+medium type "gvol") and saves both legs' per-dot stats and the metrics.  `gpu`
+rebuilds the same scene with the package's setup mirror, traces both legs with
+rb_trace_bos_pair and runs the reference's metric chain (refshim_bos_metrics,
+test infrastructure) on the B200 stats; the report compares node masks, metrics
+and per-dot displacements with the reference's.
+"""
+import json
+import os
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def reference_handle(tmpdir):
+    from oracle.oracle import Reference
+    from paper_1812_05902_b200 import scenes, setup as S
+    cfg, grid, _ = scenes.config("bos")
+    path = os.path.join(tmpdir, "bdt256.gvol")
+    S.save_gvol(grid, path)
+    cfg = json.loads(json.dumps(cfg))
+    cfg["scene"]["medium"] = {"type": "gvol", "path": path}
+    cfg["sensor"]["gain"] = 1.0
+    return Reference(json_text=json.dumps(cfg))
+
+
+def displacements(ref_hit, ref_landed, grad_hit, grad_landed):
+    ok = (ref_landed > 0) & (grad_landed > 0)
+    d = np.zeros_like(ref_hit)
+    d[ok] = grad_hit[ok] / grad_landed[ok, None] - ref_hit[ok] / ref_landed[ok, None]
+    return d, ok
+
+
+def main_ref(out):
+    with tempfile.TemporaryDirectory() as td:
+        ref = reference_handle(td)
+        scene = ref.scene()
+        t0 = time.time()
+        r0 = ref.run_trace(with_field=False, accumulate_image=False, threads=0)
+        t1 = time.time()
+        r1 = ref.run_trace(with_field=True, accumulate_image=False, threads=0)
+        t2 = time.time()
+        m = ref.bos_metrics(r0, r1)
+    np.savez_compressed(out, ref_hit=r0.hit_sum, ref_landed=r0.landed, grad_hit=r1.hit_sum,
+                        grad_landed=r1.landed, metrics=np.array(m),
+                        scene_json=np.array(json.dumps(scene.to_json())),
+                        seconds=np.array([t1 - t0, t2 - t1]),
+                        threads=np.array(r1.report["threads"]))
+    print(f"reference: {scene.n_sources} dots x {scene.rays_per_source} rays, "
+          f"{t1 - t0:.0f} s + {t2 - t1:.0f} s on {r1.report['threads']} threads; metrics {m}")
+
+
+def main_gpu(ref_npz, out_json):
+    from paper_1812_05902_b200 import scenes
+    from paper_1812_05902_b200.engine import GpuTracer
+    R = dict(np.load(ref_npz))
+    scene, grid, info, desc = scenes.build("bos")
+    same_scene = json.loads(str(R["scene_json"]))["sources"] == scene.to_json()["sources"]
+    with GpuTracer(1) as t:
+        t.set_field(grid)
+        t0 = time.time()
+        g0, g1 = t.trace_bos_pair(scene)
+        wall = time.time() - t0
+    with tempfile.TemporaryDirectory() as td:
+        ref = reference_handle(td)
+        ref_scene = ref.scene()
+        same_scene = same_scene and ref_scene.to_json() == scene.to_json()
+        m_gpu = ref.bos_metrics(g0, g1)
+
+        class _R:  # the reference's own stats through the same chain
+            def __init__(self, h, l):
+                self.hit_sum, self.landed = h, l
+        m_ref = ref.bos_metrics(_R(R["ref_hit"], R["ref_landed"]), _R(R["grad_hit"], R["grad_landed"]))
+    d_ref, ok_ref = displacements(R["ref_hit"], R["ref_landed"], R["grad_hit"], R["grad_landed"])
+    d_gpu, ok_gpu = displacements(g0.hit_sum, g0.landed, g1.hit_sum, g1.landed)
+    pitch = scene.sensor.pitch
+    both = ok_ref & ok_gpu
+    diff_px = np.abs(d_gpu[both] - d_ref[both]).max() / pitch if both.any() else 0.0
+    names = ["rms_error", "peak_abs_error", "pearson", "peak_theory", "peak_measured", "nodes"]
+    rel = {n: abs(a - b) / max(abs(b), 1e-300) for n, a, b in zip(names, m_gpu, m_ref)}
+    rep = {
+        "workload": f"bos: {scene.n_sources} dots x {scene.rays_per_source} rays, 256^3 BDT-like "
+                    "field, 1024^2 sensor (BASELINE configs[1])",
+        "same_scene_as_reference": bool(same_scene),
+        "metrics_reference": dict(zip(names, map(float, m_ref))),
+        "metrics_b200": dict(zip(names, map(float, m_gpu))),
+        "metrics_rel_diff": rel,
+        "node_count_equal": int(m_gpu[5]) == int(m_ref[5]),
+        "landed_identical": bool(np.array_equal(g1.landed, R["grad_landed"]) and
+                                 np.array_equal(g0.landed, R["ref_landed"])),
+        "valid_dots_identical": bool(np.array_equal(ok_ref, ok_gpu)),
+        "max_dot_displacement_diff_px": float(diff_px),
+        "rms_displacement_px": float(np.sqrt((d_ref[both] ** 2).sum(1).mean()) / pitch),
+        "reference_seconds": [float(x) for x in R["seconds"]],
+        "reference_threads": int(R["threads"]),
+        "b200_pair_seconds": wall,
+    }
+    with open(out_json, "w") as f:
+        json.dump(rep, f, indent=1)
+    print(json.dumps(rep, indent=1))
+    assert rep["same_scene_as_reference"] and rep["node_count_equal"] and rep["landed_identical"]
+    assert max(rel[n] for n in names[:5]) < 1e-3, rel
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "ref":
+        main_ref(sys.argv[2])
+    else:
+        main_gpu(sys.argv[2], sys.argv[3])
