@@ -66,6 +66,28 @@ def build_library(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+CHECKED_LIB = os.path.join(PKG, "libraybos_gpu_checked.so")
+
+
+def build_checked_library(verbose: bool = False) -> str:
+    """The checked build (csrc/render.cuh RB_CHECKED): the same library with every
+    K1 shared/global index range-checked, for tests/test_gpu_checked.py (the
+    pool's compute-sanitizer is closed).  Shares the host and FP64 objects."""
+    build_library(verbose)
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    objs = [os.path.join(BUILD, "capi.cpp.o"), os.path.join(BUILD, "kernels_fp64.cu.o")]
+    for src in ("kernels.cu", "kernels_nomedium.cu"):
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(BUILD, "checked_" + src + ".o")
+        objs.append(obj)
+        if _stale(obj, [path] + hdrs):
+            _run([NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-DRB_CHECKED=1",
+                  f"-I{os.path.join(ROOT, 'include')}"] + ARCH + ["-c", path, "-o", obj], verbose)
+    if _stale(CHECKED_LIB, objs):
+        _run([NVCC, "-shared"] + ARCH + objs + ["-o", CHECKED_LIB, "-ldl", "-lpthread"], verbose)
+    return CHECKED_LIB
+
+
 PEAKS_LIB = os.path.join(PKG, "libraybos_peaks.so")
 
 
@@ -101,6 +123,7 @@ def build_oracle(verbose: bool = False) -> None:
 if __name__ == "__main__":
     v = "-v" in sys.argv
     print(build_library(verbose=v, force="--force" in sys.argv))
+    print(build_checked_library(verbose=v))
     print(build_peaks(verbose=v))
     print(build_fake_nccl(verbose=v))
     build_oracle(verbose=v)

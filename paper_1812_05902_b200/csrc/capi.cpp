@@ -120,11 +120,13 @@ struct HostBuf {
 // Everything a render returns besides the image lives in one device block,
 // so a call zeroes it with one memset and reads it back with one D2H copy
 // into pinned memory: [counters u64 x8 | counters0 u64 x8 | queue, err_flag |
-// pad | hit_sum 2n f64 | landed n i64 | hit_sum0 2n | landed0 n] (the *0
-// entries only in bos pair mode).
+// check_fail x2 | hit_sum 2n f64 | landed n i64 | hit_sum0 2n | landed0 n]
+// (the *0 entries only in bos pair mode; check_fail only written by the
+// checked build).
 struct StatsLayout {
   size_t n;
-  static constexpr size_t kCounters = 0, kCounters0 = 64, kQueue = 128, kHeader = 144;
+  static constexpr size_t kCounters = 0, kCounters0 = 64, kQueue = 128, kCheck = 136,
+                          kHeader = 144;
   size_t hit() const { return kHeader; }
   size_t landed() const { return kHeader + 16 * n; }
   size_t hit0() const { return kHeader + 24 * n; }
@@ -366,6 +368,7 @@ rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, in
     k.g_mz = static_cast<float>(k.nz - 1);
     k.c_nx = static_cast<unsigned>(k.nx - 1);
     k.c_nxny = static_cast<unsigned>(k.nx - 1) * static_cast<unsigned>(k.ny - 1);
+    k.n_cells = k.c_nxny * static_cast<unsigned>(k.nz - 1);
     const double h = s->delta_xi;
     const double hs[3] = {h / k.spacing.x, h / k.spacing.y, h / k.spacing.z};
     float* dst[6][3] = {{&k.hx, &k.hy, &k.hz},    {&k.hhx, &k.hhy, &k.hhz},
@@ -464,6 +467,7 @@ struct PartialOut {
   int err_flag = 0;
   int launches = 0;  // kernels launch_on launched
   bool pair = false;
+  unsigned check_fail[2] = {0, 0};  // checked build: violations, last site code
 };
 
 // CTAs per emitter (KScene::split).  Splitting an emitter's rays over several
@@ -593,6 +597,7 @@ int launch_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   }
   k.queue = reinterpret_cast<int*>(sb + L.kQueue);
   k.err_flag = k.queue + 1;
+  k.check_fail = reinterpret_cast<unsigned*>(sb + L.kCheck);
   k.grid = dev.grid;
   k.cell_table = dev.cells;
   if (k.accumulate) {
@@ -656,6 +661,8 @@ int collect_on(rb_ctx* ctx, Device& dev, const rb_scene* s, PartialOut& po) {
     std::memcpy(po.counters0, h.as<unsigned long long>(L.kCounters0), sizeof(po.counters0));
   }
   po.err_flag = *h.as<int>(L.kQueue + sizeof(int));
+  po.check_fail[0] = *h.as<unsigned>(L.kCheck);
+  po.check_fail[1] = *h.as<unsigned>(L.kCheck + sizeof(unsigned));
   RB_CUDA(ctx, cudaEventElapsedTime(&po.ms, dev.ev0, dev.ev1));
   return RB_OK;
 }
@@ -680,6 +687,15 @@ int flag_error(rb_ctx* ctx, int flag, const rb_scene* s) {
                     " m) exceeds the fixed-point range of DotHitStats::hit_sum");
   }
   return RB_OK;
+}
+
+// The checked build's verdict (RB_CHECKED kernels; always 0 otherwise).
+int check_error(rb_ctx* ctx, const unsigned* cf) {
+  if (!cf[0]) return RB_OK;
+  return fail(ctx, RB_E_RUNTIME,
+              "checked build: " + std::to_string(cf[0]) +
+                  " out-of-range index(es) in K1, last at site " + std::to_string(cf[1]) +
+                  " (render.cuh / grin.cuh RB_CHECK)");
 }
 
 // Phase 2, the one exchange step, queued on every device's stream after its
@@ -792,8 +808,10 @@ int run_shards(rb_ctx* ctx, const rb_scene* s, const rbk::KScene& base,
         return collect_on(ctx, dev, s, parts[i]);
       }))
     return rc;
-  for (const PartialOut& po : parts)
+  for (const PartialOut& po : parts) {
+    if (int rc = check_error(ctx, po.check_fail)) return rc;
     if (po.err_flag) return flag_error(ctx, po.err_flag, s);
+  }
   return RB_OK;
 }
 
@@ -1479,6 +1497,7 @@ int rb_trace_shard(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulat
   PartialOut po;
   if (int rc = render_on(ctx, ctx->devs[0], s, base, work, reinterpret_cast<unsigned long long*>(image_fixed), po))
     return rc;
+  if (int rc = check_error(ctx, po.check_fail)) return rc;
   if (po.err_flag) return flag_error(ctx, po.err_flag, s);
   int64_t landed_total = 0;
   for (int32_t src : work) {
@@ -1547,9 +1566,10 @@ int rb_trace_rays(rb_ctx* ctx, const rb_scene* s, int with_field, int64_t n_rays
   }
   k.grid = dev.grid;
   k.cell_table = dev.cells;
-  RB_CUDA(ctx, dev.queue.ensure(sizeof(int) * 2));
-  RB_CUDA(ctx, cudaMemsetAsync(dev.queue.p, 0, sizeof(int) * 2, st));
+  RB_CUDA(ctx, dev.queue.ensure(sizeof(int) * 4));
+  RB_CUDA(ctx, cudaMemsetAsync(dev.queue.p, 0, sizeof(int) * 4, st));
   k.err_flag = dev.queue.as<int>() + 1;
+  k.check_fail = reinterpret_cast<unsigned*>(dev.queue.as<int>() + 2);
   RB_CUDA(ctx, dev.rays_src.ensure(sizeof(int64_t) * n_rays));
   RB_CUDA(ctx, dev.rays_idx.ensure(sizeof(int32_t) * n_rays));
   RB_CUDA(ctx, dev.rays_uv.ensure(sizeof(double) * 2 * n_rays));
@@ -1570,8 +1590,11 @@ int rb_trace_rays(rb_ctx* ctx, const rb_scene* s, int with_field, int64_t n_rays
   RB_CUDA(ctx, cudaMemcpyAsync(steps, dev.rays_steps.p, sizeof(int32_t) * n_rays,
                                cudaMemcpyDeviceToHost, st));
   int flag = 0;
+  unsigned cf[2] = {0, 0};
   RB_CUDA(ctx, cudaMemcpyAsync(&flag, k.err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(ctx, cudaMemcpyAsync(cf, k.check_fail, sizeof(cf), cudaMemcpyDeviceToHost, st));
   RB_CUDA(ctx, cudaStreamSynchronize(st));
+  if (int rc = check_error(ctx, cf)) return rc;
   if (flag) return flag_error(ctx, flag, s);
   return RB_OK;
 }

@@ -96,6 +96,7 @@ __device__ __forceinline__ void poly_load(const GridView& G, CellPoly& P, float 
   P.oy = oy;
   P.oz = oz;
   if (kCells) {
+    RB_CHECK(G.S, k * G.S.c_nxny + j * G.S.c_nx + i < G.S.n_cells, 6);
     const float4* c = G.S.cell_table[k * G.S.c_nxny + j * G.S.c_nx + i].c;
     P.a = __ldg(c);
     P.b = __ldg(c + 1);
@@ -107,6 +108,8 @@ __device__ __forceinline__ void poly_load(const GridView& G, CellPoly& P, float 
     P.h = __ldg(c + 7);  // (LDG.256 pairs measured 2% slower)
     return;
   }
+  RB_CHECK(G.S, (k + 1) * G.S.g_nxny + (j + 1) * G.S.g_nx + i + 1 <
+                   G.S.g_nxny * (unsigned)G.S.nz, 7);
   const float4* p0 = G.S.grid + (k * G.S.g_nxny + j * G.S.g_nx + i);
   const float4* p1 = p0 + G.S.g_nxny;
   const float4 c000 = __ldg(p0), c100 = __ldg(p0 + 1), c010 = __ldg(p0 + G.S.g_nx),
@@ -201,6 +204,8 @@ __device__ __forceinline__ float sample_nm1(const GridView& G, float qx, float q
   const float fx = __saturatef(qx - (float)i);
   const float fy = __saturatef(qy - (float)j);
   const float fz = __saturatef(qz - (float)k);
+  RB_CHECK(G.S, (k + 1) * G.S.g_nxny + (j + 1) * G.S.g_nx + i + 1 <
+                   G.S.g_nxny * (unsigned)G.S.nz, 13);
   const float* p0 = reinterpret_cast<const float*>(G.S.grid + (k * G.S.g_nxny + j * G.S.g_nx + i));
   const float* p1 = p0 + 4 * G.S.g_nxny;
   const float gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;

@@ -120,6 +120,8 @@ struct KScene {
   unsigned long long* counters;     // [0..4] lost, aperture, miss, tir, sensor_miss; [5] steps
   int* queue;                       // work counter
   int* err_flag;
+  unsigned* check_fail;             // checked build (RB_CHECKED): [0] violations, [1] last site
+  unsigned n_cells;                 // cells of the table (checked build's index bound)
   // bos_run pair mode: also follow every emitted ray without the field and
   // accumulate that leg's DotHitStats / counters here (no image)
   int32_t pair, pad_pair;

@@ -7,6 +7,28 @@
 
 #include <math.h>
 
+#ifndef RB_CHECKED
+#define RB_CHECKED 0
+#endif
+// Checked build (RB_CHECKED=1 -> libraybos_gpu_checked.so): every shared- and
+// global-memory index K1 computes is range-checked; a violation is counted in
+// check_fail[0] with its site code in check_fail[1] (no trap, the kernel
+// finishes and rb_trace reports it).  compute-sanitizer is closed on this pool;
+// this is the out-of-bounds half of its memcheck, run by tests/test_gpu_checked.py.
+#if RB_CHECKED
+#define RB_CHECK(S, cond, code)                  \
+  do {                                           \
+    if (!(cond)) {                               \
+      atomicAdd((S).check_fail, 1u);             \
+      atomicMax((S).check_fail + 1, (unsigned)(code)); \
+    }                                            \
+  } while (0)
+#else
+#define RB_CHECK(S, cond, code) \
+  do {                          \
+  } while (0)
+#endif
+
 namespace rbk {
 namespace {
 
@@ -82,10 +104,13 @@ __device__ __forceinline__ RayResult trace_ray(const KScene& S, uint64_t ekey, d
 __device__ __forceinline__ void add_px(const KScene& S, uint32_t* tile, int tc0, int tr0, int tw,
                                        int th, int c, int r, uint32_t f) {
   const int tx = c - tc0, ty = r - tr0;
-  if ((unsigned)tx < (unsigned)tw && (unsigned)ty < (unsigned)th)
+  if ((unsigned)tx < (unsigned)tw && (unsigned)ty < (unsigned)th) {
+    RB_CHECK(S, ty * tw + tx < kTileCap, 1);
     atomicAdd(&tile[ty * tw + tx], f);
-  else
+  } else {
+    RB_CHECK(S, r >= 0 && r < S.H && c >= 0 && c < S.W, 2);
     atomicAdd(&S.image[(size_t)r * S.W + c], (unsigned long long)f);
+  }
 }
 
 __device__ __forceinline__ float erf_arg(const KScene& S, int pix, double center) {
@@ -177,6 +202,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
     float e = eu0;
 #pragma unroll 1
     for (int k = 0; k < ncol; ++k) {
+      RB_CHECK(S, (k >> 2) < 3, 11);
       const float en = erff(erf_arg(S, c0 + k + 1, cc));
       reinterpret_cast<float*>(wsh + (k >> 2) * kBlock)[k & 3] = 0.5f * (en - e);
       e = en;
@@ -207,6 +233,9 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
         // The row is `width` unconditional REDs, no branch per pixel: columns
         // past the window have wu = 0, so they add floor(0 + u) = 0 to a word
         // further along the tile (the allocation has kMaxSpot words of slack).
+        RB_CHECK(S, (r - tr0) * tw + (c0 - tc0) >= 0 &&
+                        (r - tr0) * tw + (c0 - tc0) + (width <= 4 ? 4 : (width <= 8 ? 8 : kMaxSpot)) <=
+                            kTileCap + kMaxSpot, 3);
         const uint32_t trow = (uint32_t)__cvta_generic_to_shared(tile + (r - tr0) * tw + (c0 - tc0));
         float wr[kMaxSpot];
         lds_weights(wsh, wr, width <= 4 ? 1 : (width <= 8 ? 2 : 3));
@@ -348,6 +377,8 @@ __device__ __forceinline__ void place_tile(const KScene& S, int tid, int* sh_box
     sh_tile[1] = min(max(rcen - th / 2, 0), S.H - th);
     sh_tile[2] = tw;
     sh_tile[3] = th;
+    RB_CHECK(S, tw * th <= kTileCap && sh_tile[0] >= 0 && sh_tile[1] >= 0 &&
+                    sh_tile[0] + tw <= S.W && sh_tile[1] + th <= S.H, 4);
   }
   __syncthreads();
   for (int q = tid; q < sh_tile[2] * sh_tile[3]; q += kBlock) tile[q] = 0u;
@@ -407,7 +438,9 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
       const int w = atomicAdd(S.queue, 1);
       sh_work = w;
       if (w < n_units) {
+        RB_CHECK(S, w / S.split < S.n_work, 8);
         const int src = S.order[w / S.split];
+        RB_CHECK(S, src >= 0 && src < S.n_sources, 9);
         sh_src = src;
         const uint64_t sid = S.source_ids ? (uint64_t)S.source_ids[src] : (uint64_t)src;
         sh_ekey = mix_bits(S.key_seed + sid);
@@ -487,6 +520,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
         place_tile(S, tid, sh_box, sh_tile, tile);
       }
       if (r.status >= 0) {
+        RB_CHECK(S, r.status < 6, 10);
         sh_cnt[r.status][tid] += 1u;
         if (r.status == 0) {
           add_hit(S, sh_uv[0][tid], sh_uv[1][tid], r.u, r.v);
@@ -531,6 +565,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
         const uint32_t f = tile[q];
         if (f) {
           const int y = q / tw, x = q - y * tw;
+          RB_CHECK(S, tr0 + y < S.H && tc0 + x < S.W && tr0 >= 0 && tc0 >= 0, 5);
           atomicAdd(&S.image[(size_t)(tr0 + y) * S.W + (tc0 + x)], (unsigned long long)f);
         }
       }
@@ -545,6 +580,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
         for (int j = 0; j < 7; ++j) l[j] += sh_l[j][k];
       }
       const int src = sh_src;
+      RB_CHECK(S, sh_work < S.n_work * S.split, 12);
       if (S.split > 1) {
         S.hit_part[2 * (size_t)sh_work] = a;
         S.hit_part[2 * (size_t)sh_work + 1] = b;
