@@ -403,6 +403,7 @@ rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, in
   k.sigma = 0.25 * s->d_tau;                                   // sensor.cpp:65
   k.half_width = se.window_sigmas * k.sigma / se.pitch;        // sensor.cpp:79
   k.inv_s = 1.0 / (k.sigma * 1.41421356237309504880 / se.pitch);  // sensor.cpp:86
+  k.inv_s_f = static_cast<float>(k.inv_s);
   k.degenerate = k.sigma < 1e-3 * se.pitch ? 1 : 0;              // sensor.cpp:71
   k.hit_limit = std::ldexp(1.0, 22) / std::max(1, s->rays_per_source);  // render.cuh add_hit
   k.accumulate = accumulate ? 1 : 0;

@@ -112,6 +112,8 @@ struct KScene {
   int32_t W, H;
   double pitch, sigma, half_width, inv_s;
   double hit_limit;                 // |u|, |v| bound keeping a bundle's fixed-point hit sum in int64
+  float inv_s_f;                    // inv_s in FP32 (render.cuh spot_erf)
+  float pad_s;
   int32_t accumulate, degenerate;   // degenerate: sigma < 1e-3 * pitch
   // outputs
   unsigned long long* image;        // W*H fixed point (radiance * 2^31)

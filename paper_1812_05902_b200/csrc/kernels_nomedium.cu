@@ -3,8 +3,11 @@
 // raygen / optics / sensor arithmetic dominates, and here it may multiply by a
 // reciprocal instead of dividing component by component (RB_FAST_DIV,
 // stages.cuh) without perturbing the register allocation of the RK4 loop the
-// field instantiations in kernels.cu carry.
+// field instantiations in kernels.cu carry.  Likewise the spot weights use the
+// branch-free erf (RB_FAST_ERF, render.cuh: piv +5%, optics +8.5%; neutral to
+// slightly negative for the field kernels, which keep erff).
 #define RB_FAST_DIV 1
+#define RB_FAST_ERF 1
 #define RB_COMPACT_SLOW_ROWS 1
 #define RB_COMPACT_OPTICS 1
 #include "kernels.h"

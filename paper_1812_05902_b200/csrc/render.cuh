@@ -117,6 +117,61 @@ __device__ __forceinline__ float erf_arg(const KScene& S, int pix, double center
   return (float)(((double)pix - center) * S.inv_s);
 }
 
+#ifndef RB_FAST_ERF
+#define RB_FAST_ERF 0  // kernels_nomedium.cu turns it on
+#endif
+// erf for the spot weights (RB_FAST_ERF): the branch-free Chebyshev fit of erfc (Numerical
+// Recipes' erfcc, fractional error < 1.2e-7) on the MUFU reciprocal and exp2,
+// with the polynomial pre-scaled by log2(e) — about 16 instructions and no
+// divergence between lanes whose arguments fall in different ranges, against
+// erff's ~30 in several branches (erff was 27% of a no-medium ray's
+// instructions).  The weights are differences of these values normalised by
+// their own sum (sensor.cpp:106-111), so a spot's energy stays exact; a
+// per-pixel weight moves by < 1e-6 absolute.
+__device__ __forceinline__ float fast_erf(float x) {
+  const float z = fabsf(x);
+  float t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.5f, z, 1.0f)));
+  constexpr float L = 1.4426950408889634f;  // log2(e)
+  float p = 0.17087277f * L;
+  p = fmaf(p, t, -0.82215223f * L);
+  p = fmaf(p, t, 1.48851587f * L);
+  p = fmaf(p, t, -1.13520398f * L);
+  p = fmaf(p, t, 0.27886807f * L);
+  p = fmaf(p, t, -0.18628806f * L);
+  p = fmaf(p, t, 0.09678418f * L);
+  p = fmaf(p, t, 0.37409196f * L);
+  p = fmaf(p, t, 1.00002368f * L);
+  p = fmaf(p, t, -1.26551223f * L);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(z * -L, z, p)));
+  const float erfc = t * e;  // erfc(|x|)
+  return copysignf(1.0f - erfc, x);
+}
+
+// One axis of a spot window: the erf argument (pix - centre) / (sqrt2 sigma /
+// pitch) of sensor.cpp:86-95 is evaluated in FP64 once, at the window's first
+// pixel p0, and stepped by inv_s in FP32 from there.
+struct SpotAxis {
+  double center;  // spot centre in pixels (cc or rc)
+  int p0;         // first pixel of the window
+  float base;     // argument at p0
+};
+__device__ __forceinline__ SpotAxis spot_axis(const KScene& S, double center, int p0) {
+  SpotAxis a;
+  a.center = center;
+  a.p0 = p0;
+  a.base = (float)(((double)p0 - center) * S.inv_s);
+  return a;
+}
+__device__ __forceinline__ float spot_erf(const KScene& S, const SpotAxis& a, int pix) {
+#if RB_FAST_ERF
+  return fast_erf(fmaf((float)(pix - a.p0), S.inv_s_f, a.base));
+#else
+  return erff(erf_arg(S, pix, a.center));
+#endif
+}
+
 // Unbiased deterministic rounding of a fixed-point contribution: floor(x + u)
 // with a dither offset u in [0, 1) per (ray, spot row): a Weyl step of the
 // ray's counter-RNG key by the absolute row index.  Over the rays that hit a
@@ -187,9 +242,10 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
   const int cb = max(c0, 0), ce = min(c1, S.W - 1), rb = max(r0, 0), re = min(r1, S.H - 1);
   if (cb > ce || rb > re) return;
   const int ncol = c1 - c0 + 1;
-  const float eu0 = erff(erf_arg(S, c0, cc));
-  const float ev0 = erff(erf_arg(S, r0, rc));
-  const float ev1 = erff(erf_arg(S, r1 + 1, rc));
+  const SpotAxis ca = spot_axis(S, cc, c0), ra = spot_axis(S, rc, r0);
+  const float eu0 = spot_erf(S, ca, c0);
+  const float ev0 = spot_erf(S, ra, r0);
+  const float ev1 = spot_erf(S, ra, r1 + 1);
   const float mass_v = 0.5f * (ev1 - ev0);
   if (ncol <= kMaxSpot) {
     // column weights straight to shared memory, one column at a time (an
@@ -203,7 +259,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
 #pragma unroll 1
     for (int k = 0; k < ncol; ++k) {
       RB_CHECK(S, (k >> 2) < 3, 11);
-      const float en = erff(erf_arg(S, c0 + k + 1, cc));
+      const float en = spot_erf(S, ca, c0 + k + 1);
       reinterpret_cast<float*>(wsh + (k >> 2) * kBlock)[k & 3] = 0.5f * (en - e);
       e = en;
     }
@@ -216,13 +272,13 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
     // the same time instead of serialising on the same shared-memory words.
     const int nr = re - rb + 1;
     int r = rb + (int)(threadIdx.x & 31) % nr;
-    float er = r == r0 ? ev0 : erff(erf_arg(S, r, rc));
+    float er = r == r0 ? ev0 : spot_erf(S, ra, r);
     for (int jr = 0; jr < nr; ++jr, ++r) {
       if (r > re) {
         r = rb;
-        er = rb == r0 ? ev0 : erff(erf_arg(S, rb, rc));
+        er = rb == r0 ? ev0 : spot_erf(S, ra, rb);
       }
-      const float er1 = r == r1 ? ev1 : erff(erf_arg(S, r + 1, rc));
+      const float er1 = r == r1 ? ev1 : spot_erf(S, ra, r + 1);
       const float row_w = 0.5f * (er1 - er) * scale;
       const float w = row_dither(seed, r);
       er = er1;
@@ -279,18 +335,18 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
       }
     }
   } else {  // wide spots: recompute column weights per pixel
-    const float eu1 = erff(erf_arg(S, c1 + 1, cc));
+    const float eu1 = spot_erf(S, ca, c1 + 1);
     const float mass_u = 0.5f * (eu1 - eu0);
     const float scale = energy_fx / (mass_u * mass_v);
-    float er = rb == r0 ? ev0 : erff(erf_arg(S, rb, rc));
+    float er = rb == r0 ? ev0 : spot_erf(S, ra, rb);
     for (int r = rb; r <= re; ++r) {
-      const float er1 = r == r1 ? ev1 : erff(erf_arg(S, r + 1, rc));
+      const float er1 = r == r1 ? ev1 : spot_erf(S, ra, r + 1);
       const float row_w = 0.5f * (er1 - er) * scale;
       const float w = row_dither(seed, r);
       er = er1;
-      float ec = cb == c0 ? eu0 : erff(erf_arg(S, cb, cc));
+      float ec = cb == c0 ? eu0 : spot_erf(S, ca, cb);
       for (int c = cb; c <= ce; ++c) {
-        const float ec1 = c == c1 ? eu1 : erff(erf_arg(S, c + 1, cc));
+        const float ec1 = c == c1 ? eu1 : spot_erf(S, ca, c + 1);
         const uint32_t f = dround(0.5f * (ec1 - ec) * row_w, w);
         ec = ec1;
         if (f) add_px(S, tile, tc0, tr0, tw, th, c, r, f);

@@ -16,12 +16,14 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 os.makedirs(OUT, exist_ok=True)
 tag = os.environ.get("TAG", "_variant")
-obj = os.path.join(OUT, f"kernels{tag}.o")
-subprocess.run([NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", *ARCH,
-                *os.environ.get("EXTRA", "").split(), f"-I{ROOT}/include", "-c",
-                os.path.join(PKG, "csrc", "kernels.cu"), "-o", obj], check=True)
+objs = []
+for src in ("kernels.cu", "kernels_nomedium.cu"):   # both K1 translation units
+    obj = os.path.join(OUT, f"{src[:-3]}{tag}.o")
+    subprocess.run([NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", *ARCH,
+                    *os.environ.get("EXTRA", "").split(), f"-I{ROOT}/include", "-c",
+                    os.path.join(PKG, "csrc", src), "-o", obj], check=True)
+    objs.append(obj)
 lib = os.path.join(OUT, f"libraybos_gpu{tag}.so")
-others = [os.path.join(PKG, "_build", f) for f in sorted(os.listdir(os.path.join(PKG, "_build")))
-          if f.endswith(".o") and f != "kernels.cu.o"]
-subprocess.run([NVCC, "-shared", *ARCH, *others, obj, "-o", lib, "-ldl", "-lpthread"], check=True)
+others = [os.path.join(PKG, "_build", f) for f in ("capi.cpp.o", "kernels_fp64.cu.o")]
+subprocess.run([NVCC, "-shared", *ARCH, *others, *objs, "-o", lib, "-ldl", "-lpthread"], check=True)
 print(lib)
