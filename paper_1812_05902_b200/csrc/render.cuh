@@ -291,7 +291,7 @@ __device__ __forceinline__ void deposit(const KScene& S, double u, double v, uin
         // further along the tile (the allocation has kMaxSpot words of slack).
         RB_CHECK(S, (r - tr0) * tw + (c0 - tc0) >= 0 &&
                         (r - tr0) * tw + (c0 - tc0) + (width <= 4 ? 4 : (width <= 8 ? 8 : kMaxSpot)) <=
-                            kTileCap + kMaxSpot, 3);
+                            tw * th + kMaxSpot, 3);
         const uint32_t trow = (uint32_t)__cvta_generic_to_shared(tile + (r - tr0) * tw + (c0 - tc0));
         float wr[kMaxSpot];
         lds_weights(wsh, wr, width <= 4 ? 1 : (width <= 8 ? 2 : 3));
@@ -414,8 +414,18 @@ __device__ __forceinline__ void pilot_box(const KScene& S, double u, double v, i
   }
 }
 
+#ifndef RB_TILE_COPIES
+#define RB_TILE_COPIES 8
+#endif
 // Places the unit's shared tile over the pilot box (+2 px margin, at most
-// kTileCap words) and zeroes it.  Called by the whole CTA.
+// kTileCap words) and zeroes it.  Called by the whole CTA.  When the tile is
+// small it is replicated (up to RB_TILE_COPIES copies at an odd word stride)
+// and lane L deposits into copy L mod copies: the 32 rays of a coherent warp
+// land on the same pixels, so with one copy the lanes that visit the same spot
+// row at the same time hit the same words (PIV: 3.6 shared wavefronts per
+// RED), while the copies put them on different words in different banks.
+// The flush sums the copies, so the image is unchanged.
+// sh_tile: tc0, tr0, tw, th, copies, stride.
 __device__ __forceinline__ void place_tile(const KScene& S, int tid, int* sh_box, int* sh_tile,
                                            uint32_t* tile) {
   __syncthreads();
@@ -433,11 +443,18 @@ __device__ __forceinline__ void place_tile(const KScene& S, int tid, int* sh_box
     sh_tile[1] = min(max(rcen - th / 2, 0), S.H - th);
     sh_tile[2] = tw;
     sh_tile[3] = th;
+    const int stride = (tw * th + kMaxSpot) | 1;
+    int copies = 1;
+    while (copies < RB_TILE_COPIES && 2 * copies * stride <= kTileCap + kMaxSpot) copies *= 2;
+    sh_tile[4] = copies;
+    sh_tile[5] = copies > 1 ? stride : 0;
     RB_CHECK(S, tw * th <= kTileCap && sh_tile[0] >= 0 && sh_tile[1] >= 0 &&
-                    sh_tile[0] + tw <= S.W && sh_tile[1] + th <= S.H, 4);
+                    sh_tile[0] + tw <= S.W && sh_tile[1] + th <= S.H &&
+                    (copies == 1 || copies * stride <= kTileCap + kMaxSpot), 4);
   }
   __syncthreads();
-  for (int q = tid; q < sh_tile[2] * sh_tile[3]; q += kBlock) tile[q] = 0u;
+  const int words = sh_tile[4] > 1 ? sh_tile[4] * sh_tile[5] : sh_tile[2] * sh_tile[3];
+  for (int q = tid; q < words; q += kBlock) tile[q] = 0u;
   __syncthreads();
 }
 
@@ -463,7 +480,7 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
   constexpr int kWarps = kBlock / 32;
   __shared__ int sh_work, sh_src;
   __shared__ int sh_box[4];
-  __shared__ int sh_tile[4];                 // tc0, tr0, tw, th
+  __shared__ int sh_tile[6];                 // tc0, tr0, tw, th, copies, stride (place_tile)
   __shared__ double sh_so[3];                // emitter position
   __shared__ unsigned long long sh_ekey;     // per-emitter RNG key
   // Per-thread emitter accumulators and the GRIN entry state live in shared
@@ -506,7 +523,8 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
       }
       sh_box[0] = sh_box[1] = 0x7fffffff;
       sh_box[2] = sh_box[3] = -1;
-      sh_tile[0] = sh_tile[1] = sh_tile[2] = sh_tile[3] = 0;
+      sh_tile[0] = sh_tile[1] = sh_tile[2] = sh_tile[3] = sh_tile[5] = 0;
+      sh_tile[4] = 1;
     }
     sh_uv[0][tid] = sh_uv[1][tid] = 0ll;
     sh_uv0[0][tid] = sh_uv0[1][tid] = 0ll;
@@ -581,7 +599,8 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
         if (r.status == 0) {
           add_hit(S, sh_uv[0][tid], sh_uv[1][tid], r.u, r.v);
           if (S.accumulate)
-            deposit(S, r.u, r.v, tile, vtile[0], vtile[1], vtile[2], vtile[3],
+            deposit(S, r.u, r.v, tile + (lane & (vtile[4] - 1)) * vtile[5], vtile[0], vtile[1],
+                    vtile[2], vtile[3],
                     (uint32_t)(mix_bits(ekey + (uint64_t)i) >> 32), wsh);
         }
       }
@@ -617,8 +636,10 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
     __syncthreads();
     if (S.accumulate) {  // flush the tile (composite_tile, engine.cpp:181-187)
       const int tc0 = sh_tile[0], tr0 = sh_tile[1], tw = sh_tile[2], th = sh_tile[3];
+      const int copies = sh_tile[4], stride = sh_tile[5];
       for (int q = tid; q < tw * th; q += kBlock) {
-        const uint32_t f = tile[q];
+        uint32_t f = tile[q];
+        for (int c = 1; c < copies; ++c) f += tile[c * stride + q];
         if (f) {
           const int y = q / tw, x = q - y * tw;
           RB_CHECK(S, tr0 + y < S.H && tc0 + x < S.W && tr0 >= 0 && tc0 >= 0, 5);

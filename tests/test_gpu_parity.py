@@ -53,8 +53,15 @@ def test_per_ray_hits_match_reference(tracer, name, with_field):
     ok = status == 0
     err_px = np.abs(uv[ok] - g[f"ray_uv_{with_field}"][ok]).max(initial=0.0) / scene.sensor.pitch
     assert err_px < PX_TOL, err_px
-    # step counts may differ by one where a step ends within rounding of a face
-    assert np.abs(steps - g[f"ray_steps_{with_field}"]).max(initial=0) <= 1
+    # A step count can differ by one only where a step ends within FP32 rounding
+    # of a box face (the in-box test runs on the FP32 grid-unit state, the
+    # reference's box.contains on FP64, grin.cpp:101): bound it AND count it.
+    d = np.abs(steps - g[f"ray_steps_{with_field}"])
+    assert d.max(initial=0) <= 1
+    n_diff = int((d > 0).sum())
+    assert n_diff <= max(1, steps.size // 1000), (n_diff, steps.size)   # observed: 0
+    if n_diff:
+        print(f"{name}: {n_diff} of {steps.size} rays differ by one RK4 step")
 
 
 @pytest.mark.parametrize("name", ["field3d", "shock_particles"])
