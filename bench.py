@@ -163,6 +163,16 @@ def profiled_traffic(scene: str):
         return None
 
 
+def profiled_instructions(scene: str):
+    """K1 warp instructions per ray of this scene from the committed ncu capture
+    (profiles/k1_instructions.json: smsp__inst_executed.sum / rays of one launch)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_instructions.json")) as f:
+            return json.load(f).get(scene)
+    except OSError:
+        return None
+
+
 def measured_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -468,6 +478,19 @@ def bench_scene(job, name, scale, steps, warmup, args, want_cpu, want_e2e):
 
     peaks = measure_peaks(dev0)
     n_gpus = len(job.devices) * job.world
+    ins = profiled_instructions(name)
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    sms = job.torch.cuda.get_device_properties(dev0).multi_processor_count
+    peak_issue = 4.0 * sms * sm_mhz * 1e6 / 1e9  # G warp-instructions / s
+    issue = None
+    if ins:
+        ach = ins["warp_inst_per_ray"] * rays_total / n_gpus / (kms * 1e-3) / 1e9
+        issue = {"achieved": ach, "peak": peak_issue, "unit": "Gwarp-inst/s",
+                 "frac": ach / peak_issue,
+                 "per_ray": f"{ins['warp_inst_per_ray']:.1f} warp-instructions per ray "
+                            f"({ins['source']})",
+                 "peak_source": f"4 warp-instructions/clk/SM x {sms} SMs x {sm_mhz:.0f} MHz "
+                                "(the SM clock sampled during the timed steps)"}
     if grid is not None:
         flops = FLOPS_PER_STEP * steps_sum + FLOPS_PER_RAY * rays_total
         achieved = flops / n_gpus / (kms * 1e-3) / 1e12
@@ -483,20 +506,28 @@ def bench_scene(job, name, scale, steps, warmup, args, want_cpu, want_e2e):
                     # which is why K1 caches the cell in registers instead
                     "gather": {"uncached_equivalent_gbs": gather,
                                "l2_gather_peak_gbs": peaks["l2_gather_gbs"],
-                               "bytes_per_step": GATHER_BYTES_PER_STEP}}
+                               "bytes_per_step": GATHER_BYTES_PER_STEP},
+                    "issue": issue}
     else:
+        # Without a medium K1 is instruction-issue bound (SURVEY §8(d) names the
+        # deposition, but its shared REDs run at < 10% of their measured peak):
+        # the roof is the SMs' issue rate, 4 warp-instructions per clock per SM
+        # at the clock measured during the timed steps, and the work is the
+        # committed ncu count of warp-instructions per ray of this scene.
         landed = res.report["landed"]
         reds = spot_reds_per_ray(scene) * landed
-        achieved = reds / n_gpus / (kms * 1e-3) / 1e9
-        roofline = {"bound": "smem_red", "achieved": achieved, "peak": peaks["red_shared_gops"],
-                    "unit": "Gop/s", "frac": achieved / peaks["red_shared_gops"],
-                    "per_ray": f"{spot_reds_per_ray(scene):.1f} shared-memory RED.ADD.U32 per "
-                               f"landed ray (spot window (2 hw + 1)^2); {landed} of "
-                               f"{rays_total} rays landed",
-                    "peak_source": "measured on this box: conflict-free red.shared.add.u32 "
-                                   "microbenchmark (tools/peaks.cu)",
-                    "fp32_tflops_equivalent": (FLOPS_PER_RAY * rays_total / n_gpus /
-                                               (kms * 1e-3) / 1e12)}
+        red_ach = reds / n_gpus / (kms * 1e-3) / 1e9
+        deposition = {"achieved": red_ach, "peak": peaks["red_shared_gops"], "unit": "Gop/s",
+                      "frac": red_ach / peaks["red_shared_gops"],
+                      "per_ray": f"{spot_reds_per_ray(scene):.1f} shared-memory RED.ADD.U32 per "
+                                 f"landed ray (spot window (2 hw + 1)^2); {landed} of "
+                                 f"{rays_total} rays landed",
+                      "peak_source": "measured on this box: conflict-free red.shared.add.u32 "
+                                     "microbenchmark (tools/peaks.cu)"}
+        if issue:
+            roofline = dict(issue, bound="issue", deposition=deposition)
+        else:
+            roofline = dict(deposition, bound="smem_red")
     roofline.update({"traffic": profiled_traffic(name) if n_gpus == 1 else None,
                      "traffic_source": "profiles/k1_traffic.json (ncu --set full, one launch)",
                      "kernel": "render_emitters", "kernel_ms": kms,

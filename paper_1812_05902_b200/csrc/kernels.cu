@@ -14,6 +14,12 @@
 // fixed-point sum (radiance * 2^31) and the DotHitStats sums are fixed point too,
 // so every output is order-independent and bit-identical for any emitter order,
 // chunking, CTA count or GPU count.
+// FP64 normalisations by one reciprocal (stages.cuh RB_FAST_DIV) and the
+// branch-free spot erf (render.cuh RB_FAST_ERF), as in kernels_nomedium.cu:
+// together tomo +1.5%, bos neutral, with the RK4 loop's allocation unchanged
+// (242 instructions, no spills).  The FP64 validation build keeps neither.
+#define RB_FAST_DIV 1
+#define RB_FAST_ERF 1
 #include "kernels.h"
 #include "render.cuh"
 

@@ -1,11 +1,10 @@
 // kernels_nomedium.cu — K1 for scenes without a medium (render_emitters with
-// kField = 0 and its per-ray replay), compiled apart from kernels.cu: its FP64
-// raygen / optics / sensor arithmetic dominates, and here it may multiply by a
-// reciprocal instead of dividing component by component (RB_FAST_DIV,
-// stages.cuh) without perturbing the register allocation of the RK4 loop the
-// field instantiations in kernels.cu carry.  Likewise the spot weights use the
-// branch-free erf (RB_FAST_ERF, render.cuh: piv +5%, optics +8.5%; neutral to
-// slightly negative for the field kernels, which keep erff).
+// kField = 0 and its per-ray replay), compiled apart from kernels.cu so its
+// code-size choices (rolled off-tile spot rows and thick-lens surfaces,
+// RB_COMPACT_*: the no-medium kernel is instruction-cache bound) cannot perturb
+// the register allocation of the RK4 loop the field instantiations carry.
+// Both units use the FP64 reciprocal normalisations (RB_FAST_DIV, stages.cuh)
+// and the branch-free spot erf (RB_FAST_ERF, render.cuh: piv +5%, optics +8.5%).
 #define RB_FAST_DIV 1
 #define RB_FAST_ERF 1
 #define RB_COMPACT_SLOW_ROWS 1

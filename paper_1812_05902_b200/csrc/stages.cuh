@@ -17,10 +17,10 @@ __device__ __forceinline__ double3 operator-(double3 a, double3 b) {
 __device__ __forceinline__ double3 operator*(double3 a, double s) {
   return make_double3(a.x * s, a.y * s, a.z * s);
 }
-// RB_FAST_DIV (the no-medium K1, kernels_nomedium.cu): one reciprocal and three
+// RB_FAST_DIV (K1, kernels.cu and kernels_nomedium.cu): one reciprocal and three
 // multiplies instead of three FP64 divisions (they were 9% of a no-medium
-// render); ≤1 ulp per component, ~1e-17 m at the sensor.  Everywhere else the
-// components are divided as the reference does.
+// render); ≤1 ulp per component, ~1e-17 m at the sensor.  The FP64 validation
+// build (kernels_fp64.cu) divides the components as the reference does.
 __device__ __forceinline__ double3 operator/(double3 a, double s) {
 #if RB_FAST_DIV
   const double inv = 1.0 / s;

@@ -59,8 +59,10 @@ def main_ref(out):
         r1 = ref.run_trace(with_field=True, accumulate_image=False, threads=0)
         t2 = time.time()
         m = ref.bos_metrics(r0, r1)
+    names = ["rms_error", "peak_abs_error", "pearson", "peak_theory", "peak_measured", "nodes"]
     np.savez_compressed(out, ref_hit=r0.hit_sum, ref_landed=r0.landed, grad_hit=r1.hit_sum,
-                        grad_landed=r1.landed, metrics=np.array(m),
+                        grad_landed=r1.landed, metrics=np.array([float(m[n]) for n in names]),
+                        metric_names=np.array(names),
                         scene_json=np.array(json.dumps(scene.to_json())),
                         seconds=np.array([t1 - t0, t2 - t1]),
                         threads=np.array(r1.report["threads"]))
@@ -82,7 +84,9 @@ def main_gpu(ref_npz, out_json):
     with tempfile.TemporaryDirectory() as td:
         ref = reference_handle(td)
         ref_scene = ref.scene()
-        same_scene = same_scene and ref_scene.to_json() == scene.to_json()
+        a, b = ref_scene.to_json(), scene.to_json()
+        a.pop("config_hash"), b.pop("config_hash")  # physics_hash of the GVOL config only
+        same_scene = same_scene and a == b
         m_gpu = ref.bos_metrics(g0, g1)
 
         class _R:  # the reference's own stats through the same chain
@@ -95,13 +99,17 @@ def main_gpu(ref_npz, out_json):
     both = ok_ref & ok_gpu
     diff_px = np.abs(d_gpu[both] - d_ref[both]).max() / pitch if both.any() else 0.0
     names = ["rms_error", "peak_abs_error", "pearson", "peak_theory", "peak_measured", "nodes"]
+    m_gpu = [float(m_gpu[n]) for n in names]
+    m_ref = [float(m_ref[n]) for n in names]
+    m_saved = [float(x) for x in R["metrics"]]
     rel = {n: abs(a - b) / max(abs(b), 1e-300) for n, a, b in zip(names, m_gpu, m_ref)}
     rep = {
         "workload": f"bos: {scene.n_sources} dots x {scene.rays_per_source} rays, 256^3 BDT-like "
                     "field, 1024^2 sensor (BASELINE configs[1])",
         "same_scene_as_reference": bool(same_scene),
-        "metrics_reference": dict(zip(names, map(float, m_ref))),
-        "metrics_b200": dict(zip(names, map(float, m_gpu))),
+        "metrics_reference": dict(zip(names, m_ref)),
+        "metrics_reference_as_run": dict(zip(names, m_saved)),
+        "metrics_b200": dict(zip(names, m_gpu)),
         "metrics_rel_diff": rel,
         "node_count_equal": int(m_gpu[5]) == int(m_ref[5]),
         "landed_identical": bool(np.array_equal(g1.landed, R["grad_landed"]) and
