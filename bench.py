@@ -153,14 +153,18 @@ def measure_peaks(device: int) -> dict:
     return _PEAKS[device]
 
 
-def profiled_traffic(scene: str):
+def profiled_traffic(scene: str, rays: float):
     """dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch of this
-    scene, from the committed ncu capture (profiles/k1_traffic.json), or None."""
+    scene from the committed ncu capture (profiles/k1_traffic.json), scaled to
+    `rays` when the capture traced fewer (the 1024^3 share), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
-            return json.load(f).get(scene, {}).get("dram_bytes_per_launch")
+            t = json.load(f).get(scene)
     except OSError:
         return None
+    if not t:
+        return None
+    return t["dram_bytes_per_launch"] * rays / t.get("rays_per_launch", rays)
 
 
 def profiled_instructions(scene: str):
@@ -528,8 +532,9 @@ def bench_scene(job, name, scale, steps, warmup, args, want_cpu, want_e2e):
             roofline = dict(issue, bound="issue", deposition=deposition)
         else:
             roofline = dict(deposition, bound="smem_red")
-    roofline.update({"traffic": profiled_traffic(name) if n_gpus == 1 else None,
-                     "traffic_source": "profiles/k1_traffic.json (ncu --set full, one launch)",
+    roofline.update({"traffic": profiled_traffic(name, rays_total) if n_gpus == 1 else None,
+                     "traffic_source": "profiles/k1_traffic.json (ncu --set full of one K1 "
+                                       "launch, per ray x this launch's rays)",
                      "kernel": "render_emitters", "kernel_ms": kms,
                      "ffma_reg_tflops": peaks["ffma_reg_tflops"],
                      "ffma_imm_tflops": peaks["ffma_imm_tflops"],

@@ -197,7 +197,9 @@ int rb_create_devices(const int* devices, int n_devices, rb_ctx** out, char* err
  * this rank's shard of the SAME scene (all ranks pass the same scene), the
  * library sums the partial images onto rank 0 with one ncclReduce and
  * all-reduces the per-source stats and counters, so every rank returns the
- * whole call's DotHitStats and RunReport and rank 0 also returns the image. */
+ * whole call's DotHitStats and RunReport and rank 0 also returns the image.
+ * With world == 1 an id is optional; given one, the one-rank job still runs
+ * the NCCL exchange (a single-GPU check of the collective path). */
 #define RB_NCCL_UNIQUE_ID_BYTES 128
 int rb_nccl_unique_id(void* id, size_t len, char* err, size_t errlen);
 int rb_create_rank(int device, int rank, int world, const void* id, size_t len, rb_ctx** out,

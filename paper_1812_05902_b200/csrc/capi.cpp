@@ -241,6 +241,7 @@ struct rb_ctx {
   // way every device of every process takes part in every collective.
   std::vector<ncclComm_t> comms;
   int rank = 0, world = 1;
+  bool rank_mode = false;  // rb_create_rank made a communicator (also for a one-rank job)
   ShardPlan plan;
 };
 
@@ -711,7 +712,7 @@ int exchange(rb_ctx* ctx, const rb_scene* s, bool image, bool pair) {
   NcclApi& api = ctx->nccl;
   const size_t n = static_cast<size_t>(s->n_sources);
   const size_t npx = static_cast<size_t>(s->sensor.width_px) * s->sensor.height_px;
-  const bool dist = ctx->world > 1;
+  const bool dist = ctx->rank_mode;
   if (!image && !dist) return RB_OK;
   if (api.group_start() != ncclSuccess) return fail(ctx, RB_E_CUDA, "ncclGroupStart failed");
   ncclResult_t r = ncclSuccess;
@@ -795,14 +796,14 @@ int run_shards(rb_ctx* ctx, const rb_scene* s, const rbk::KScene& base,
   const ShardPlan& plan = shard_plan(ctx, s);
   work = plan.work;
   parts.assign(nd, PartialOut{});
-  const bool dist = ctx->world > 1;
+  const bool dist = ctx->rank_mode;
   const double f_in = base.with_field ? plan.f_in : 0.0;
   if (int rc = for_each_device(ctx, [&](Device& dev) -> int {
         const size_t i = static_cast<size_t>(&dev - ctx->devs.data());
         return launch_on(ctx, dev, s, base, work[i], nullptr, dist, true, f_in, parts[i]);
       }))
     return rc;
-  if (static_cast<int64_t>(nd) * ctx->world > 1)
+  if (static_cast<int64_t>(nd) * ctx->world > 1 || ctx->rank_mode)
     if (int rc = exchange(ctx, s, base.accumulate != 0, base.pair != 0)) return rc;
   if (int rc = for_each_device(ctx, [&](Device& dev) -> int {
         const size_t i = static_cast<size_t>(&dev - ctx->devs.data());
@@ -833,7 +834,7 @@ void merge_stats(const rb_ctx* ctx, const rb_scene* s,
     if (landed) landed[src] = l[src];
     landed_total += l[src];
   };
-  if (ctx->world > 1) {  // all-reduced: device 0 holds every source and the totals
+  if (ctx->rank_mode) {  // all-reduced: device 0 holds every source and the totals
     const PartialOut& po = parts[0];
     for (int32_t src = 0; src < static_cast<int32_t>(s->n_sources); ++src) take(po, src);
     for (int j = 0; j < 6; ++j) c[j] = leg0 ? po.counters0[j] : po.counters[j];
@@ -1122,11 +1123,16 @@ int rb_create_rank(int device, int rank, int world, const void* id, size_t len, 
     return fail(nullptr, RB_E_INVALID, "rb_create_rank: bad rank/world", err, errlen);
   if (world > 1 && (!id || len < sizeof(ncclUniqueId)))
     return fail(nullptr, RB_E_INVALID, "rb_create_rank: missing ncclUniqueId", err, errlen);
+  if (id && len < sizeof(ncclUniqueId))
+    return fail(nullptr, RB_E_INVALID, "rb_create_rank: ncclUniqueId too short", err, errlen);
   if (int rc = make_ctx(&device, 1, out, err, errlen)) return rc;
   rb_ctx* ctx = *out;
   ctx->rank = rank;
   ctx->world = world;
-  if (world > 1) {
+  // A communicator whenever an id is given, also for a one-rank job: the rank-mode
+  // exchange then runs against the real NCCL on a single GPU (nothing waits on
+  // another rank), which is how the collective calls are exercised on this pool.
+  if (world > 1 || id) {
     std::string msg;
     if (!ctx->nccl.load(msg)) {
       *out = nullptr;
@@ -1138,6 +1144,7 @@ int rb_create_rank(int device, int rank, int world, const void* id, size_t len, 
     ctx->comms.assign(1, nullptr);
     cudaSetDevice(device);
     const ncclResult_t r = ctx->nccl.init_rank(&ctx->comms[0], world, u, rank);
+    if (r == ncclSuccess) ctx->rank_mode = true;
     if (r != ncclSuccess) {
       ctx->comms.clear();
       *out = nullptr;

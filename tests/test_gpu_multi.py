@@ -178,3 +178,30 @@ def test_real_nccl_rank_mode(tmp_path):
     res = _run_ranks("blob", 2, tmp_path, {"RAYBOS_NCCL_LIB": ""})
     assert np.array_equal(res[0]["image"], ref.image)
     assert np.array_equal(res[1]["hit_sum"], ref.hit_sum)
+
+
+@pytest.mark.parametrize("name", ["blob", "small", "singlet_defocus", "shock_particles"])
+def test_real_nccl_one_rank_job(monkeypatch, name):
+    """rb_create_rank(world = 1) with an id builds a real one-rank NCCL
+    communicator, so the rank-mode exchange (image ncclReduce + the all-reduces of
+    stats, counters and error flag, grouped on the device stream) runs against the
+    real libnccl on one GPU — nothing waits on another rank."""
+    monkeypatch.delenv("RAYBOS_NCCL_LIB", raising=False)
+    from golden_io import load
+    from paper_1812_05902_b200.engine import GpuTracer, nccl_unique_id
+    ref = _single(name)
+    scene, field, _ = load(name)
+    t = GpuTracer.for_rank(0, 0, 1, nccl_unique_id())
+    try:
+        info = t.comm_info()
+        assert info["comm_ranks"] == 1 and info["world"] == 1 and info["nccl_version"] > 0
+        t.set_field(field)
+        _same(t.run_trace(scene), ref)
+        if field is not None:
+            with GpuTracer(1) as t1:
+                t1.set_field(field)
+                a0, a1 = t1.trace_bos_pair(scene)
+            b0, b1 = t.trace_bos_pair(scene)
+            assert np.array_equal(a0.hit_sum, b0.hit_sum) and np.array_equal(a1.hit_sum, b1.hit_sum)
+    finally:
+        t.close()
