@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -790,8 +791,12 @@ const ShardPlan& shard_plan(rb_ctx* ctx, const rb_scene* s) {
   return p;
 }
 
+// tail: optional work queued on device 0 of rank 0 after the exchange and
+// before the stats readback (rb_trace's image copies), so one stream sync covers
+// both.
 int run_shards(rb_ctx* ctx, const rb_scene* s, const rbk::KScene& base,
-               std::vector<std::vector<int32_t>>& work, std::vector<PartialOut>& parts) {
+               std::vector<std::vector<int32_t>>& work, std::vector<PartialOut>& parts,
+               const std::function<int(Device&)>& tail = nullptr) {
   const int nd = static_cast<int>(ctx->devs.size());
   const ShardPlan& plan = shard_plan(ctx, s);
   work = plan.work;
@@ -805,6 +810,8 @@ int run_shards(rb_ctx* ctx, const rb_scene* s, const rbk::KScene& base,
     return rc;
   if (static_cast<int64_t>(nd) * ctx->world > 1 || ctx->rank_mode)
     if (int rc = exchange(ctx, s, base.accumulate != 0, base.pair != 0)) return rc;
+  if (tail && ctx->rank == 0)
+    if (int rc = tail(ctx->devs[0])) return rc;
   if (int rc = for_each_device(ctx, [&](Device& dev) -> int {
         const size_t i = static_cast<size_t>(&dev - ctx->devs.data());
         return collect_on(ctx, dev, s, parts[i]);
@@ -1439,18 +1446,10 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
   const rbk::KScene base = make_kscene(ctx, s, with_field, accumulate_image);
   std::vector<std::vector<int32_t>> work;
   std::vector<PartialOut> parts;
-  if (int rc = run_shards(ctx, s, base, work, parts)) return rc;
-  unsigned long long c[6];
-  int64_t landed_total = 0;
-  merge_stats(ctx, s, work, parts, false, out->hit_sum, out->landed, c, landed_total);
-  float ms = 0.f;
-  int launches = 0;
-  for (const PartialOut& po : parts) {
-    ms = std::max(ms, po.ms);
-    launches += po.launches;
-  }
-  if (accumulate_image && root && (out->image || out->quantized || out->image_fixed)) {
-    Device& d0 = ctx->devs[0];
+  int tail_launches = 0;
+  // the image tail on device 0, queued before the stats readback's stream sync
+  auto tail = [&](Device& d0) -> int {
+    if (!(accumulate_image && (out->image || out->quantized || out->image_fixed))) return RB_OK;
     RB_CUDA(ctx, cudaSetDevice(d0.ordinal));
     if (out->image_fixed)  // device-resident result: the reduced fixed-point image
       RB_CUDA(ctx, cudaMemcpyAsync(out->image_fixed, d0.image.p, npx * sizeof(uint64_t),
@@ -1460,7 +1459,7 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
       RB_CUDA(ctx, rbk::launch_image_finalize(d0.image.as<unsigned long long>(),
                                               d0.dimage.as<double>(), static_cast<int64_t>(npx),
                                               d0.stream));
-      ++launches;
+      ++tail_launches;
       if (out->image)
         RB_CUDA(ctx, cudaMemcpyAsync(out->image, d0.dimage.p, npx * sizeof(double),
                                      cudaMemcpyDeviceToHost, d0.stream));
@@ -1469,12 +1468,22 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
         RB_CUDA(ctx, rbk::launch_quantize(d0.dimage.as<double>(), static_cast<int64_t>(npx),
                                           out->gain, out->bit_depth, d0.qimage.as<uint16_t>(),
                                           d0.stream));
-        ++launches;
+        ++tail_launches;
         RB_CUDA(ctx, cudaMemcpyAsync(out->quantized, d0.qimage.p, npx * sizeof(uint16_t),
                                      cudaMemcpyDeviceToHost, d0.stream));
       }
     }
-    RB_CUDA(ctx, cudaStreamSynchronize(d0.stream));
+    return RB_OK;
+  };
+  if (int rc = run_shards(ctx, s, base, work, parts, tail)) return rc;
+  unsigned long long c[6];
+  int64_t landed_total = 0;
+  merge_stats(ctx, s, work, parts, false, out->hit_sum, out->landed, c, landed_total);
+  float ms = 0.f;
+  int launches = tail_launches;
+  for (const PartialOut& po : parts) {
+    ms = std::max(ms, po.ms);
+    launches += po.launches;
   }
   fill_report(out, s, s->n_sources, c, landed_total);
   out->threads = total;
