@@ -109,7 +109,7 @@ EXPORTED_SYMBOLS = (
     "rb_trace", "rb_plan_shards", "rb_trace_shard", "rb_image_from_fixed", "rb_trace_rays",
     "rb_trace_rays_fp64", "rb_trace_stats_fp64", "rb_trace_debug", "rb_trace_bos_pair",
     "rb_set_field_gvol", "rb_create_devices", "rb_nccl_unique_id", "rb_create_rank",
-    "rb_comm_info",
+    "rb_comm_info", "rb_plan_reset", "rb_host_alloc", "rb_host_free",
 )
 RB_NCCL_UNIQUE_ID_BYTES = 128
 
@@ -139,6 +139,12 @@ def load_library(path: str | None = None) -> C.CDLL:
     lib.rb_create_rank.restype = C.c_int
     lib.rb_comm_info.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 4
     lib.rb_comm_info.restype = C.c_int
+    lib.rb_plan_reset.argtypes = [C.c_void_p]
+    lib.rb_plan_reset.restype = C.c_int
+    lib.rb_host_alloc.argtypes = [C.c_size_t]
+    lib.rb_host_alloc.restype = C.c_void_p
+    lib.rb_host_free.argtypes = [C.c_void_p]
+    lib.rb_host_free.restype = None
     lib.rb_destroy.argtypes = [C.c_void_p]
     lib.rb_destroy.restype = None
     lib.rb_last_error.argtypes = [C.c_void_p]

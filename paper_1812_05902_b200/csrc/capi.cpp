@@ -1182,6 +1182,26 @@ void rb_destroy(rb_ctx* ctx) {
   if (ctx) destroy_ctx(ctx);
 }
 
+int rb_plan_reset(rb_ctx* ctx) {
+  if (!ctx) return RB_E_INVALID;
+  ctx->plan.valid = false;
+  for (Device& d : ctx->devs) d.plan_on_device = false;
+  return RB_OK;
+}
+
+void* rb_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void rb_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, const double* gx,
                        const double* gy, const double* gz) {
   if (!ctx) return RB_E_INVALID;

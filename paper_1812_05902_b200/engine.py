@@ -95,6 +95,27 @@ class GpuTracer:
         if self.ctx:
             self.lib.rb_destroy(self.ctx)
             self.ctx = C.c_void_p()
+        for p in getattr(self, "_pinned", []):
+            self.lib.rb_host_free(p)
+        self._pinned = []
+
+    def pinned(self, shape, dtype=np.float64) -> np.ndarray:
+        """A numpy array in page-locked host memory (rb_host_alloc), owned by
+        this tracer (freed by close): pass it as run_trace's image_out so the
+        image comes back at full copy bandwidth."""
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = self.lib.rb_host_alloc(n)
+        if not p:
+            raise RaybosError("rb_host_alloc failed")
+        if not hasattr(self, "_pinned"):
+            self._pinned = []
+        self._pinned.append(p)
+        buf = (C.c_char * n).from_address(p)
+        return np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def reset_plan(self):
+        """rb_plan_reset: the next run_trace re-plans and re-uploads the sources."""
+        self.lib.rb_plan_reset(self.ctx)
 
     def __del__(self):
         try:
