@@ -129,9 +129,13 @@ _PEAKS = {}
 
 
 def measure_peaks(device: int) -> dict:
-    """The roofline denominators, measured on this box (tools/peaks.cu)."""
+    """The roofline denominators, measured on this box (tools/peaks.cu), with
+    the SM clocks sampled while the microbenchmarks ran."""
     if device in _PEAKS:
         return _PEAKS[device]
+    sampler = ClockSampler([device])
+    sampler.start()
+    time.sleep(0.3)
     from paper_1812_05902_b200 import build as b
     lib = C.CDLL(b.PEAKS_LIB)
     for fn in ("rbp_ffma_tflops",):
@@ -150,6 +154,7 @@ def measure_peaks(device: int) -> dict:
                       "l2_gather_gbs": lib.rbp_l2_gather_gbs(device, 64.0),
                       "red_shared_gops": lib.rbp_red_shared_gops(device),
                       "dfma_tflops": lib.rbp_dfma_tflops(device)}
+    _PEAKS[device]["clocks"] = sampler.stop()
     return _PEAKS[device]
 
 
@@ -550,7 +555,9 @@ def bench_scene(job, name, scale, steps, warmup, args, want_cpu, want_e2e):
                      "ffma2_tflops": peaks["ffma2_tflops"],
                      "red_shared_gops": peaks["red_shared_gops"],
                      "dfma_tflops": peaks["dfma_tflops"],
-                     "hbm_gbs_measured": measured_hbm(), "peak_clocks": clocks})
+                     "hbm_gbs_measured": measured_hbm(),
+                     "peak_clocks": peaks["clocks"],   # during the peak microbenchmarks
+                     "kernel_clocks": clocks})         # during the timed steps
     cpu = None
     if want_cpu:
         try:
