@@ -354,15 +354,22 @@ class Job:
         self.device = local if self.backend == "nccl" else local % ndev
         torch.cuda.set_device(self.device)
         from paper_1812_05902_b200.engine import GpuTracer, nccl_unique_id
-        if world > 1:
-            if self.backend == "nccl":
-                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+        if world > 1 or "WORLD_SIZE" in os.environ:
+            # launched by torchrun: one process per GPU, the library's rank mode —
+            # also for a one-process run, so every N of a scaling curve goes
+            # through the same rb_create_rank + NCCL exchange path
+            if world > 1:
+                if self.backend == "nccl":
+                    dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+                else:
+                    dist.init_process_group(self.backend)
+                uid = [nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(uid, src=0)
             else:
-                dist.init_process_group(self.backend)
-            uid = [nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
+                uid = [nccl_unique_id()]
             self.tracer = GpuTracer.for_rank(self.device, rank, world, uid[0])
             self.devices = [self.device]
+            self.mode = "ranks"
         elif args.gpus > 1:
             # RAYBOS_BENCH_DEVICES (path check only, e.g. "0,0" on a one-GPU box
             # with the NCCL stand-in) names the devices; default 0..N-1
@@ -370,9 +377,11 @@ class Job:
             self.devices = ([int(x) for x in env.split(",")] if env else list(range(args.gpus)))
             assert len(self.devices) == args.gpus
             self.tracer = GpuTracer(devices=self.devices)
+            self.mode = "in-process"
         else:
             self.tracer = GpuTracer(n_devices=1, first_device=self.device)
             self.devices = [self.device]
+            self.mode = "single"
         self.comm = self.tracer.comm_info()
         print(f"raybos: rank {rank} of {world} process(es), devices {self.devices}, NCCL "
               f"communicator spans {self.comm['comm_ranks']} rank(s)"
@@ -603,8 +612,7 @@ def main_ours(args, rank, world, local):
                 "roofline": head["roofline"], "cpu_baseline": head["cpu_baseline"],
                 "clocks": head["clocks"], "gpu_launches": head["gpu_launches"],
                 "image_checksum": head["image_checksum"],
-                "comm": dict(job.comm, mode=("ranks" if job.world > 1 else
-                                             ("in-process" if n_gpus > 1 else "single")),
+                "comm": dict(job.comm, mode=job.mode,
                              processes=job.world, devices_per_process=len(job.devices))}
         if extras:
             line["configs"] = extras
