@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -33,6 +34,17 @@
 namespace {
 
 constexpr int kShardTile = 32;  // consecutive (Z-ordered) sources per shard tile
+
+// NVTX range for the duration of a scope (header-only NVTX 3: free unless a
+// tool such as Nsight Systems attaches), so the host phases of a call — shard
+// plan, launches, the exchange, the readback, field builds — line up with the
+// kernels on a timeline.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Device allocation owned by one Device (move-only; freed on destruction, on
 // the device it was allocated on), so early error returns cannot leak it.
@@ -554,6 +566,7 @@ int for_each_device(rb_ctx* ctx, F&& fn) {
 int launch_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& base,
               const std::vector<int32_t>& work, unsigned long long* image_target, bool zero_stats,
               bool use_plan, double f_in, PartialOut& po) {
+  NvtxRange nvtx_("raybos launch");
   RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
   const int64_t n = s->n_sources;
   const size_t npx = static_cast<size_t>(s->sensor.width_px) * s->sensor.height_px;
@@ -646,6 +659,7 @@ int launch_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
 // Phase 3: per-source stats, counters and the error flag to the host, then
 // wait for the device's stream (which also covers any collective queued on it).
 int collect_on(rb_ctx* ctx, Device& dev, const rb_scene* s, PartialOut& po) {
+  NvtxRange nvtx_("raybos readback");
   RB_CUDA(ctx, cudaSetDevice(dev.ordinal));
   const int64_t n = s->n_sources;
   const StatsLayout L{static_cast<size_t>(n)};
@@ -710,6 +724,7 @@ int check_error(rb_ctx* ctx, const unsigned* cf) {
 // statistics.  Stats entries have one non-zero contributor and the image is
 // an integer, so every sum is exact: bit-identical for any device count.
 int exchange(rb_ctx* ctx, const rb_scene* s, bool image, bool pair) {
+  NvtxRange nvtx_("raybos exchange (NCCL)");
   NcclApi& api = ctx->nccl;
   const size_t n = static_cast<size_t>(s->n_sources);
   const size_t npx = static_cast<size_t>(s->sensor.width_px) * s->sensor.height_px;
@@ -756,6 +771,7 @@ int exchange(rb_ctx* ctx, const rb_scene* s, bool image, bool pair) {
 // them (exchange).  Every device takes part even when its shard is empty, so
 // the collectives always see every rank.
 const ShardPlan& shard_plan(rb_ctx* ctx, const rb_scene* s) {
+  NvtxRange nvtx_("raybos shard plan");
   ShardPlan& p = ctx->plan;
   const size_t n = static_cast<size_t>(s->n_sources);
   const bool same =
@@ -1204,6 +1220,7 @@ void rb_host_free(void* p) {
 
 int rb_set_field_nodes(rb_ctx* ctx, const rb_field_desc* desc, const double* n, const double* gx,
                        const double* gy, const double* gz) {
+  NvtxRange nvtx_("raybos set_field_nodes");
   if (!ctx) return RB_E_INVALID;
   if (int rc = check_field_desc(ctx, desc)) return rc;
   if (!n || !gx || !gy || !gz) return fail(ctx, RB_E_INVALID, "rb_set_field_nodes: NULL array");
@@ -1275,6 +1292,7 @@ bool valid_density(const float* rho, size_t n) {  // DensityVolume::validate, sc
 
 int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rho,
                          double gladstone_dale_k) {
+  NvtxRange nvtx_("raybos set_field_density");
   if (!ctx) return RB_E_INVALID;
   if (int rc = check_field_desc(ctx, desc)) return rc;
   if (!rho) return fail(ctx, RB_E_INVALID, "rb_set_field_density: rho is NULL");
@@ -1304,6 +1322,7 @@ int rb_set_field_density(rb_ctx* ctx, const rb_field_desc* desc, const float* rh
 // (open, header, dims/spacing, truncation, then DensityVolume::validate).
 int rb_set_field_gvol(rb_ctx* ctx, const char* path, const double* z_center,
                       double gladstone_dale_k, int64_t slab_bytes, rb_field_desc* desc_out) {
+  NvtxRange nvtx_("raybos set_field_gvol");
   if (!ctx) return RB_E_INVALID;
   if (!path) return fail(ctx, RB_E_INVALID, "rb_set_field_gvol: path is NULL");
   const std::string p(path);
@@ -1433,6 +1452,7 @@ int64_t rb_field_bytes(const rb_ctx* ctx) {
 
 int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_image,
              rb_trace_out* out) {
+  NvtxRange nvtx_("raybos rb_trace");
   if (!ctx || !out) return RB_E_INVALID;
   const auto t0 = std::chrono::steady_clock::now();
   if (int rc = validate_scene(ctx, s)) return rc;
@@ -1815,6 +1835,7 @@ extern "C" int rb_trace_debug(rb_ctx* ctx, const rb_scene* s, int64_t source_ind
 
 extern "C" int rb_trace_bos_pair(rb_ctx* ctx, const rb_scene* s, rb_trace_out* out_ref,
                                  rb_trace_out* out_grad) {
+  NvtxRange nvtx_("raybos rb_trace_bos_pair");
   if (!ctx || !out_ref || !out_grad) return RB_E_INVALID;
   const auto t0 = std::chrono::steady_clock::now();
   if (int rc = validate_scene(ctx, s)) return rc;
