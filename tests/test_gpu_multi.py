@@ -205,3 +205,19 @@ def test_real_nccl_one_rank_job(monkeypatch, name):
             assert np.array_equal(a0.hit_sum, b0.hit_sum) and np.array_equal(a1.hit_sum, b1.hit_sum)
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("name,scale", [("tomo", 0.005), ("bos", 0.02)])
+def test_bench_scene_on_three_devices_bit_identical(fake_nccl, name, scale):
+    """A bench scene with emitter splitting (tomo 8, bos 25 CTAs per emitter),
+    the cell table and the shard-plan cache, on three in-process devices."""
+    from paper_1812_05902_b200 import scenes
+    from paper_1812_05902_b200.engine import GpuTracer
+    scene, grid, info, desc = scenes.build(name, scale=scale)
+    with GpuTracer(n_devices=1) as t1:
+        t1.set_field(grid)
+        ref = t1.run_trace(scene)
+    with GpuTracer(devices=[0, 0, 0]) as t:
+        t.set_field(grid)
+        for _ in range(2):                       # second call: cached plan on every device
+            _same(t.run_trace(scene), ref)
