@@ -766,10 +766,10 @@ int exchange(rb_ctx* ctx, const rb_scene* s, bool image, bool pair) {
   return RB_OK;
 }
 
-// Renders this process's shards — device d of rank r takes shard r * nd + d
-// of world * nd, from the same Z-order plan as rb_plan_shards — and combines
-// them (exchange).  Every device takes part even when its shard is empty, so
-// the collectives always see every rank.
+// The cached shard plan for this scene (ShardPlan), rebuilt when the sources,
+// stream ids or pupil axis differ from the previous call's: device d of rank r
+// takes shard r * nd + d of world * nd, from the same Z-order plan as
+// rb_plan_shards.
 const ShardPlan& shard_plan(rb_ctx* ctx, const rb_scene* s) {
   NvtxRange nvtx_("raybos shard plan");
   ShardPlan& p = ctx->plan;
@@ -807,7 +807,9 @@ const ShardPlan& shard_plan(rb_ctx* ctx, const rb_scene* s) {
   return p;
 }
 
-// tail: optional work queued on device 0 of rank 0 after the exchange and
+// Renders this process's shards and combines them (exchange).  Every device
+// takes part even when its shard is empty, so the collectives always see every
+// rank.  tail: optional work queued on device 0 of rank 0 after the exchange and
 // before the stats readback (rb_trace's image copies), so one stream sync covers
 // both.
 int run_shards(rb_ctx* ctx, const rb_scene* s, const rbk::KScene& base,
