@@ -525,7 +525,11 @@ int emitter_split(const rb_ctx* ctx, const rb_scene* s, const rbk::KScene& k, si
   }
   if (n_work > 0 && n_work < static_cast<size_t>(resident_ctas))
     split = std::max(split, std::ceil(2.0 * resident_ctas / static_cast<double>(n_work)));
-  return static_cast<int>(std::max(1.0, std::min(static_cast<double>(cap), split)));
+  // K1 gives each chunk ceil(iters / split) patch iterations; trim the split to
+  // the chunks that then have work (bos: 25 -> 20, five empty units per emitter)
+  const int sp = static_cast<int>(std::max(1.0, std::min(static_cast<double>(cap), split)));
+  const int per = (iters + sp - 1) / sp;
+  return (iters + per - 1) / per;
 }
 
 // One device renders the given work list into dev.image (already zeroed or
