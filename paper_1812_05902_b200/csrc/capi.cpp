@@ -632,6 +632,23 @@ int launch_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   if (k.with_field && !dev.grid) return fail(ctx, RB_E_RUNTIME, "rb_trace: field not uploaded");
   k.split = emitter_split(ctx, s, k, work.size(),
                           dev.sms * dev.blocks_per_sm[k.pair ? 1 : 0][rbk::field_mode(k)], f_in);
+  {
+    // K1 variant for field scenes (not the bos pair): render_warps (warp-level
+    // work items, no CTA barriers) when the emitters sit outside the volume
+    // (dots: bos +2.5%, 1024^3 +1.7%), render_emitters when they sit inside it
+    // (tomo particles: the warps of a CTA then share one emitter's cells; the
+    // warp variant's independent items drop tomo's L1 hit rate from 90% to 54%
+    // and thrash the instruction cache, -10%).  RAYBOS_K1=cta|warp overrides.
+    const char* e = std::getenv("RAYBOS_K1");
+    const bool want_warp = e && *e ? (e[0] == 'w') : (f_in < 0.5);
+    if (want_warp && k.with_field && !k.pair) {
+      k.warp_mode = 1;
+      const int warps = rbk::kBlock / 32;
+      const int want = std::max(1, std::min(k.patch_count, k.split * warps));
+      const int per = (k.patch_count + want - 1) / want;
+      k.split = (k.patch_count + per - 1) / per;  // items per emitter
+    }
+  }
   if (k.split > 1) {
     const size_t units = work.size() * static_cast<size_t>(k.split);
     RB_CUDA(ctx, dev.hit_part.ensure(sizeof(long long) * 2 * units));

@@ -23,9 +23,12 @@
 // The field scenes' spots are in focus (~12 px windows): a 2048-word tile (8 KB
 // instead of 24 KB) leaves more of the SM's L1 to the cell table (+0.2%); the
 // no-medium kernel keeps 6144 words for defocused spots.
+#ifndef RB_TILE_CAP
 #define RB_TILE_CAP 2048
+#endif
 #include "kernels.h"
 #include "render.cuh"
+#include "render_warps.cuh"
 
 namespace rbk {
 namespace {
@@ -168,6 +171,10 @@ int render_occupancy(int blocks_per_sm[2][3]) {
   set_smem<false, 2>();
   set_smem<true, 1>();
   set_smem<true, 2>();
+  cudaFuncSetAttribute(render_warps<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)render_smem());
+  cudaFuncSetAttribute(render_warps<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)render_smem());
   blocks_per_sm[0][1] = occupancy<false, 1>();
   blocks_per_sm[0][2] = occupancy<false, 2>();
   blocks_per_sm[1][1] = occupancy<true, 1>();
@@ -186,8 +193,14 @@ cudaError_t launch_render(const KScene& s, int grid, cudaStream_t stream) {
   switch (field_mode(s) + (s.pair ? 3 : 0)) {
     case 0:
     case 3: return launch_render_nomedium(s, grid, stream);  // kernels_nomedium.cu
-    case 1: render_emitters<false, 1><<<grid, kBlock, sm, stream>>>(s); break;
-    case 2: render_emitters<false, 2><<<grid, kBlock, sm, stream>>>(s); break;
+    case 1:
+      if (s.warp_mode) render_warps<1><<<grid, kBlock, sm, stream>>>(s);
+      else render_emitters<false, 1><<<grid, kBlock, sm, stream>>>(s);
+      break;
+    case 2:
+      if (s.warp_mode) render_warps<2><<<grid, kBlock, sm, stream>>>(s);
+      else render_emitters<false, 2><<<grid, kBlock, sm, stream>>>(s);
+      break;
     case 4: render_emitters<true, 1><<<grid, kBlock, sm, stream>>>(s); break;
     default: render_emitters<true, 2><<<grid, kBlock, sm, stream>>>(s); break;
   }

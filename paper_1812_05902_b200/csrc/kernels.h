@@ -134,7 +134,8 @@ struct KScene {
   // in flight -> a smaller L2 working set); each writes its DotHitStats partial
   // to part[work * split + chunk] and emitter_stats_kernel sums them in chunk
   // order (deterministic).  split == 1 writes hit_sum / landed directly.
-  int32_t split, pad_split;
+  int32_t split;
+  int32_t warp_mode;                // 1: render_warps (warp-level items; split = items per emitter)
   long long* hit_part;              // 2 * n_work * split, fixed point (render.cuh kHitScale)
   long long* landed_part;
   long long* hit_part0;

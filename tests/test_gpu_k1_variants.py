@@ -1,0 +1,39 @@
+"""The two K1 work distributions — render_emitters (CTA-level chunks, chosen
+when the emitters sit inside the volume) and render_warps (warp-level items,
+chosen for emitters outside it) — must give the same integers: the image,
+DotHitStats, counters and RK4 step totals, bit for bit (RAYBOS_K1 forces one)."""
+import numpy as np
+import pytest
+
+from golden_io import NAMES, load
+
+pytestmark = pytest.mark.gpu
+FIELD = [n for n in NAMES if load(n)[1] is not None]
+
+
+def _run(tracer, scene, mode, monkeypatch):
+    monkeypatch.setenv("RAYBOS_K1", mode)
+    return tracer.run_trace(scene, True, True)
+
+
+@pytest.mark.parametrize("name", FIELD)
+def test_warp_items_equal_cta_chunks(tracer, name, monkeypatch):
+    scene, field, g = load(name)
+    tracer.set_field(field)
+    a = _run(tracer, scene, "cta", monkeypatch)
+    b = _run(tracer, scene, "warp", monkeypatch)
+    assert np.array_equal(a.image, b.image)
+    assert np.array_equal(a.hit_sum, b.hit_sum) and np.array_equal(a.landed, b.landed)
+    for k in ("lost", "blocked_aperture", "blocked_miss", "blocked_tir", "blocked_sensor_miss",
+              "total_steps"):
+        assert a.report[k] == b.report[k], k
+
+
+@pytest.mark.parametrize("name,scale", [("bos", 0.02), ("tomo", 0.003)])
+def test_warp_items_equal_cta_chunks_on_bench_scenes(tracer, name, scale, monkeypatch):
+    from paper_1812_05902_b200 import scenes
+    scene, grid, info, desc = scenes.build(name, scale=scale)
+    tracer.set_field(grid)
+    a = _run(tracer, scene, "cta", monkeypatch)
+    b = _run(tracer, scene, "warp", monkeypatch)
+    assert np.array_equal(a.image, b.image) and np.array_equal(a.hit_sum, b.hit_sum)
