@@ -26,7 +26,7 @@ N GPUs, either way the driver launches it:
               synchronous call; max over ranks.
   e2e         the same call with HOST buffers: the FP64 image and the stats
               copied to the host every step (sources H2D every step in both).
-  roofline    K1 render_emitters: scenes with a medium against the box's
+  roofline    K1 (render_emitters / render_warps, as the call reports): scenes with a medium against the box's
               measured FP32 FFMA peak (tools/peaks.cu; MEASURED_PEAKS.json
               has no CUDA-core figure), algorithmic work 360 flops per RK4
               step + 700 per ray; scenes without a medium
@@ -156,6 +156,10 @@ def measure_peaks(device: int) -> dict:
                       "dfma_tflops": lib.rbp_dfma_tflops(device)}
     _PEAKS[device]["clocks"] = sampler.stop()
     return _PEAKS[device]
+
+
+# rb_trace_out::k1_kernel -> the render kernel that ran (include/raybos_gpu.h)
+K1_NAMES = {1: "render_emitters", 2: "render_warps"}
 
 
 def profiled_traffic(scene: str, rays: float):
@@ -558,7 +562,8 @@ def bench_scene(job, name, scale, steps, warmup, args, want_cpu, want_e2e):
     roofline.update({"traffic": profiled_traffic(name, rays_total) if n_gpus == 1 else None,
                      "traffic_source": "profiles/k1_traffic.json (ncu --set full of one K1 "
                                        "launch, per ray x this launch's rays)",
-                     "kernel": "render_emitters", "kernel_ms": kms,
+                     "kernel": K1_NAMES.get(res.report.get("k1_kernel", 1), "render_emitters"),
+                     "kernel_ms": kms,
                      "ffma_reg_tflops": peaks["ffma_reg_tflops"],
                      "ffma_imm_tflops": peaks["ffma_imm_tflops"],
                      "ffma2_tflops": peaks["ffma2_tflops"],

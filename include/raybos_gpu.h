@@ -77,7 +77,8 @@ typedef struct rb_surface {
 
 typedef struct rb_element {
   int32_t kind; /* RB_ELEM_* */
-  int32_t reserved;
+  int32_t k1_kernel; /* out: the render kernel that ran: 1 render_emitters, 2 render_warps
+                        (0: no sources) */
   /* aperture: center, axis = normal, radius.
    * thin lens: center, axis, focal_length, diameter. */
   rb_vec3 center;
@@ -135,7 +136,8 @@ typedef struct rb_scene {
  * (i,j,k) sits at origin + (i*dx, j*dy, k*dz), x-fastest storage. */
 typedef struct rb_field_desc {
   int32_t nx, ny, nz;
-  int32_t reserved;
+  int32_t k1_kernel; /* out: the render kernel that ran: 1 render_emitters, 2 render_warps
+                        (0: no sources) */
   rb_vec3 origin;
   rb_vec3 spacing;
 } rb_field_desc;
@@ -157,7 +159,8 @@ typedef struct rb_trace_out {
   int64_t blocked_sensor_miss;
   double wall_seconds;
   int32_t threads; /* devices used (RunReport::threads)                         */
-  int32_t reserved;
+  int32_t k1_kernel; /* out: the render kernel that ran: 1 render_emitters, 2 render_warps
+                        (0: no sources) */
   uint64_t config_hash;
   /* instrumentation (not in the reference report) */
   int64_t total_steps;     /* sum of RK4 steps over all rays                   */

@@ -62,7 +62,7 @@ class TraceOut(C.Structure):
                 ("emitted", C.c_int64), ("landed_total", C.c_int64), ("lost", C.c_int64),
                 ("blocked_aperture", C.c_int64), ("blocked_miss", C.c_int64),
                 ("blocked_tir", C.c_int64), ("blocked_sensor_miss", C.c_int64),
-                ("wall_seconds", C.c_double), ("threads", C.c_int32), ("reserved", C.c_int32),
+                ("wall_seconds", C.c_double), ("threads", C.c_int32), ("k1_kernel", C.c_int32),
                 ("config_hash", C.c_uint64), ("total_steps", C.c_int64),
                 ("kernel_ms", C.c_double), ("quantized", C.POINTER(C.c_uint16)),
                 ("gain", C.c_double), ("bit_depth", C.c_int32), ("kernel_launches", C.c_int32),

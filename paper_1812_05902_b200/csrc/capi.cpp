@@ -481,6 +481,7 @@ struct PartialOut {
   float ms = 0.f;
   int err_flag = 0;
   int launches = 0;  // kernels launch_on launched
+  int k1 = 0;        // rb_trace_out::k1_kernel of this launch
   bool pair = false;
   unsigned check_fail[2] = {0, 0};  // checked build: violations, last site code
 };
@@ -649,6 +650,7 @@ int launch_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
       k.split = (k.patch_count + per - 1) / per;  // items per emitter
     }
   }
+  po.k1 = k.warp_mode ? 2 : 1;
   if (k.split > 1) {
     const size_t units = work.size() * static_cast<size_t>(k.split);
     RB_CUDA(ctx, dev.hit_part.ensure(sizeof(long long) * 2 * units));
@@ -1491,6 +1493,7 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
   const bool root = ctx->rank == 0;  // the image lands on rank 0, device 0
   out->kernel_ms = 0.0;
   out->kernel_launches = 0;
+  out->k1_kernel = 0;
   if (s->n_sources == 0) {  // engine.cpp:436: one "thread", blank image, no stats
     if (accumulate_image && root) {
       if (out->image) std::memset(out->image, 0, npx * sizeof(double));
@@ -1544,12 +1547,15 @@ int rb_trace(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate_imag
   merge_stats(ctx, s, work, parts, false, out->hit_sum, out->landed, c, landed_total);
   float ms = 0.f;
   int launches = tail_launches;
+  int k1 = 0;
   for (const PartialOut& po : parts) {
     ms = std::max(ms, po.ms);
     launches += po.launches;
+    k1 = std::max(k1, po.k1);
   }
   fill_report(out, s, s->n_sources, c, landed_total);
   out->threads = total;
+  out->k1_kernel = k1;
   out->kernel_ms = ms;
   out->kernel_launches = launches;
   out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1566,6 +1572,7 @@ int rb_trace_shard(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulat
   if (int rc = validate_scene(ctx, s)) return rc;
   const unsigned long long zero[6] = {0, 0, 0, 0, 0, 0};
   out->threads = 1;
+  out->k1_kernel = 0;
   if (s->n_sources == 0) {
     fill_report(out, s, 0, zero, 0);
     return RB_OK;
@@ -1591,6 +1598,7 @@ int rb_trace_shard(rb_ctx* ctx, const rb_scene* s, int with_field, int accumulat
   fill_report(out, s, static_cast<int64_t>(work.size()), po.counters, landed_total);
   out->kernel_ms = po.ms;
   out->kernel_launches = po.launches;
+  out->k1_kernel = po.k1;
   out->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return RB_OK;
 }
@@ -1777,6 +1785,7 @@ extern "C" int rb_trace_stats_fp64(rb_ctx* ctx, const rb_scene* s, int with_fiel
   if (int rc = validate_scene(ctx, s)) return rc;
   const unsigned long long zero[6] = {0, 0, 0, 0, 0, 0};
   out->threads = 1;
+  out->k1_kernel = 0;
   out->kernel_ms = 0.0;
   if (s->n_sources == 0) {
     fill_report(out, s, 0, zero, 0);
@@ -1904,6 +1913,7 @@ extern "C" int rb_trace_bos_pair(rb_ctx* ctx, const rb_scene* s, rb_trace_out* o
   out_ref->threads = out_grad->threads = static_cast<int>(ctx->devs.size()) * ctx->world;
   out_ref->kernel_ms = out_grad->kernel_ms = ms;
   out_ref->kernel_launches = out_grad->kernel_launches = launches;
+  out_ref->k1_kernel = out_grad->k1_kernel = 1;
   out_ref->wall_seconds = out_grad->wall_seconds = wall;
   return RB_OK;
 }

@@ -340,4 +340,5 @@ def report_from(out: abi.TraceOut) -> dict:
             "blocked_tir": out.blocked_tir, "blocked_sensor_miss": out.blocked_sensor_miss,
             "wall_seconds": out.wall_seconds, "threads": out.threads,
             "config_hash": out.config_hash, "total_steps": out.total_steps,
-            "kernel_ms": out.kernel_ms, "kernel_launches": out.kernel_launches}
+            "kernel_ms": out.kernel_ms, "kernel_launches": out.kernel_launches,
+            "k1_kernel": out.k1_kernel}

@@ -11,9 +11,14 @@ pytestmark = pytest.mark.gpu
 FIELD = [n for n in NAMES if load(n)[1] is not None]
 
 
-def _run(tracer, scene, mode, monkeypatch):
+CODE = {"cta": 1, "warp": 2}
+
+
+def _run(tracer, scene, monkeypatch):
     monkeypatch.setenv("RAYBOS_K1", mode)
-    return tracer.run_trace(scene, True, True)
+    r = tracer.run_trace(scene, True, True)
+    assert r.report["k1_kernel"] == CODE[mode]
+    return r
 
 
 @pytest.mark.parametrize("name", FIELD)
@@ -21,7 +26,7 @@ def test_warp_items_equal_cta_chunks(tracer, name, monkeypatch):
     scene, field, g = load(name)
     tracer.set_field(field)
     a = _run(tracer, scene, "cta", monkeypatch)
-    b = _run(tracer, scene, "warp", monkeypatch)
+    b = _run(tracer, scene, monkeypatch)
     assert np.array_equal(a.image, b.image)
     assert np.array_equal(a.hit_sum, b.hit_sum) and np.array_equal(a.landed, b.landed)
     for k in ("lost", "blocked_aperture", "blocked_miss", "blocked_tir", "blocked_sensor_miss",
@@ -35,5 +40,16 @@ def test_warp_items_equal_cta_chunks_on_bench_scenes(tracer, name, scale, monkey
     scene, grid, info, desc = scenes.build(name, scale=scale)
     tracer.set_field(grid)
     a = _run(tracer, scene, "cta", monkeypatch)
-    b = _run(tracer, scene, "warp", monkeypatch)
+    b = _run(tracer, scene, monkeypatch)
     assert np.array_equal(a.image, b.image) and np.array_equal(a.hit_sum, b.hit_sum)
+
+
+@pytest.mark.parametrize("name,scale,code", [("bos", 0.02, 2), ("tomo", 0.003, 1)])
+def test_default_variant_follows_emitter_placement(tracer, name, scale, code, monkeypatch):
+    """Emitters outside the volume (bos dots) -> render_warps, inside (tomo
+    particles) -> render_emitters; the call reports which one ran."""
+    from paper_1812_05902_b200 import scenes
+    monkeypatch.delenv("RAYBOS_K1", raising=False)
+    scene, grid, info, desc = scenes.build(name, scale=scale)
+    tracer.set_field(grid)
+    assert tracer.run_trace(scene, True, True).report["k1_kernel"] == code
