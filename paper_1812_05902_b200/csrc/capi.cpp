@@ -636,7 +636,7 @@ int launch_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   {
     // K1 variant for field scenes (not the bos pair): render_warps (warp-level
     // work items, no CTA barriers) when the emitters sit outside the volume
-    // (dots: bos +2.5%, 1024^3 +1.7%), render_emitters when they sit inside it
+    // (dots: bos +1-2%, 1024^3 +0-0.7% at full scale), render_emitters when they sit inside it
     // (tomo particles: the warps of a CTA then share one emitter's cells; the
     // warp variant's independent items drop tomo's L1 hit rate from 90% to 54%
     // and thrash the instruction cache, -10%).  RAYBOS_K1=cta|warp overrides.
