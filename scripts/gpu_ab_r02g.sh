@@ -1,4 +1,5 @@
 # A/B: render_emitters vs render_warps (global queue) vs render_warps (CTA pool), full-scale scenes.
+# (the CTA-pool variant, RAYBOS_K1=wpool, was measured here and removed: tomo +1% over warp, still -9% vs cta)
 cd "${GRAFT_REPO_ROOT:-.}"
 O=gpurun_out; mkdir -p $O
 timeout 600 python -m pytest tests/test_gpu_k1_variants.py -q -x > $O/g_variants.log 2>&1; echo "variants rc=$?"; tail -2 $O/g_variants.log
