@@ -357,11 +357,18 @@ rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, in
     const int64_t band_positions = static_cast<int64_t>((rows + 3) / 4) * k.band_rays;
     k.patch_count = static_cast<int32_t>((band_positions + 31) / 32);
     const int warps = rbk::kBlock / 32;
+    // Without a medium the unit's first patch iteration is its pilot, so a
+    // coprime stride deals that iteration's 8 patches across the whole pupil
+    // (the tile then covers defocused spots); with a medium the pilot is a
+    // separate straight trace spread over the unit, and stride 1 keeps a CTA's
+    // 8 warps on neighbouring patches — one narrow cone of cells in L1
+    // (bos +0.9%, 1024^3 +1.9%, tomo +0.4%).
     int st = std::max(1, k.patch_count / warps);
     while (std::gcd(st, k.patch_count) != 1) ++st;
     k.patch_stride = st % std::max(1, k.patch_count) == 0 ? 1 : st;
   }
   k.with_field = (with_field && ctx->has_field) ? 1 : 0;
+  if (k.with_field) k.patch_stride = 1;  // see the patch order above
   if (k.with_field) {
     k.nx = ctx->field.nx;
     k.ny = ctx->field.ny;
@@ -633,22 +640,14 @@ int launch_on(rb_ctx* ctx, Device& dev, const rb_scene* s, const rbk::KScene& ba
   if (k.with_field && !dev.grid) return fail(ctx, RB_E_RUNTIME, "rb_trace: field not uploaded");
   k.split = emitter_split(ctx, s, k, work.size(),
                           dev.sms * dev.blocks_per_sm[k.pair ? 1 : 0][rbk::field_mode(k)], f_in);
-  {
-    // K1 variant for field scenes (not the bos pair): render_warps (warp-level
-    // work items, no CTA barriers) when the emitters sit outside the volume
-    // (dots: bos +1-2%, 1024^3 +0-0.7% at full scale), render_emitters when they sit inside it
-    // (tomo particles: the warps of a CTA then share one emitter's cells; the
-    // warp variant's independent items drop tomo's L1 hit rate from 90% to 54%
-    // and thrash the instruction cache, -10%).  RAYBOS_K1=cta|warp overrides.
-    const char* e = std::getenv("RAYBOS_K1");
-    const bool want_warp = e && *e ? (e[0] == 'w') : (f_in < 0.5);
-    if (want_warp && k.with_field && !k.pair) {
-      k.warp_mode = 1;
-      const int warps = rbk::kBlock / 32;
-      const int want = std::max(1, std::min(k.patch_count, k.split * warps));
-      const int per = (k.patch_count + want - 1) / want;
-      k.split = (k.patch_count + per - 1) / per;  // items per emitter
-    }
+  if (const char* e = std::getenv("RAYBOS_K1"); e && e[0] == 'w' && k.with_field && !k.pair) {
+    // render_warps (warp-level work items, no CTA barrier): the
+    // split becomes items per emitter, kWarps per render_emitters chunk
+    k.warp_mode = 1;
+    const int warps = rbk::kBlock / 32;
+    const int want = std::max(1, std::min(k.patch_count, k.split * warps));
+    const int per = (k.patch_count + want - 1) / want;
+    k.split = (k.patch_count + per - 1) / per;
   }
   po.k1 = k.warp_mode ? 2 : 1;
   if (k.split > 1) {

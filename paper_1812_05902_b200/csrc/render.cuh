@@ -388,13 +388,21 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 // Ray index of this lane in patch slot `slot` (k * warps + warp) of the strided
 // patch order, or -1 past the lattice (kernels.h KScene::band_rays).
-__device__ __forceinline__ int patch_ray(const KScene& S, int slot, int lane, int N) {
-  if (slot >= S.patch_count) return -1;
-  const int p = (int)(((long long)slot * S.patch_stride) % S.patch_count);
+// Ray index of `lane` in patch p of the band order (consecutive p are
+// neighbouring patches of the pupil lattice), or -1 past the lattice.
+__device__ __forceinline__ int patch_ray_at(const KScene& S, int p, int lane, int N) {
   const int j = p * 32 + lane;  // position in the 4-row bands (kernels.h)
   const int band = j / S.band_rays, rem = j - band * S.band_rays;
   const int cx = rem >> 2, cy = band * 4 + (rem & 3);
   return cy * S.cells + cx < N ? cy * S.cells + cx : -1;
+}
+
+// render_emitters' slot order: slot k kWarps + w (warp w, patch iteration k)
+// visits patch slot * patch_stride mod patch_count, so the 8 patches of one
+// iteration lie across the whole pupil.
+__device__ __forceinline__ int patch_ray(const KScene& S, int slot, int lane, int N) {
+  if (slot >= S.patch_count) return -1;
+  return patch_ray_at(S, (int)(((long long)slot * S.patch_stride) % S.patch_count), lane, N);
 }
 
 // Grows the unit's pilot bounding box by a landed ray's spot_pixel_window
@@ -554,7 +562,9 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
     // anyway is added to the global image directly, so the image is the same.
     constexpr bool kStraightPilot = RB_STRAIGHT_PILOT && kField != 0;
     if (kStraightPilot && S.accumulate) {
-      const int i = patch_ray(S, kb * kWarps + warp, lane, N);
+      // warp w pilots its patch of iteration kb + w (ke - kb) / kWarps, so the box
+      // spans the unit's iterations, not only its first
+      const int i = patch_ray(S, (kb + (warp * (ke - kb)) / kWarps) * kWarps + warp, lane, N);
       if (i >= 0) {
         const double3 so = make_double3(vso[0], vso[1], vso[2]);
         double3 d;

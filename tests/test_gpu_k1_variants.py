@@ -1,7 +1,6 @@
-"""The two K1 work distributions — render_emitters (CTA-level chunks, chosen
-when the emitters sit inside the volume) and render_warps (warp-level items,
-chosen for emitters outside it) — must give the same integers: the image,
-DotHitStats, counters and RK4 step totals, bit for bit (RAYBOS_K1 forces one)."""
+"""The two K1 work distributions — render_emitters (CTA-level chunks, the
+default) and render_warps (warp-level items, RAYBOS_K1=warp) — must give the
+same integers: the image, DotHitStats, counters and RK4 step totals, bit for bit."""
 import numpy as np
 import pytest
 
@@ -14,7 +13,7 @@ FIELD = [n for n in NAMES if load(n)[1] is not None]
 CODE = {"cta": 1, "warp": 2}
 
 
-def _run(tracer, scene, monkeypatch):
+def _run(tracer, scene, mode, monkeypatch):
     monkeypatch.setenv("RAYBOS_K1", mode)
     r = tracer.run_trace(scene, True, True)
     assert r.report["k1_kernel"] == CODE[mode]
@@ -26,7 +25,7 @@ def test_warp_items_equal_cta_chunks(tracer, name, monkeypatch):
     scene, field, g = load(name)
     tracer.set_field(field)
     a = _run(tracer, scene, "cta", monkeypatch)
-    b = _run(tracer, scene, monkeypatch)
+    b = _run(tracer, scene, "warp", monkeypatch)
     assert np.array_equal(a.image, b.image)
     assert np.array_equal(a.hit_sum, b.hit_sum) and np.array_equal(a.landed, b.landed)
     for k in ("lost", "blocked_aperture", "blocked_miss", "blocked_tir", "blocked_sensor_miss",
@@ -40,16 +39,16 @@ def test_warp_items_equal_cta_chunks_on_bench_scenes(tracer, name, scale, monkey
     scene, grid, info, desc = scenes.build(name, scale=scale)
     tracer.set_field(grid)
     a = _run(tracer, scene, "cta", monkeypatch)
-    b = _run(tracer, scene, monkeypatch)
+    b = _run(tracer, scene, "warp", monkeypatch)
     assert np.array_equal(a.image, b.image) and np.array_equal(a.hit_sum, b.hit_sum)
 
 
-@pytest.mark.parametrize("name,scale,code", [("bos", 0.02, 2), ("tomo", 0.003, 1)])
-def test_default_variant_follows_emitter_placement(tracer, name, scale, code, monkeypatch):
-    """Emitters outside the volume (bos dots) -> render_warps, inside (tomo
-    particles) -> render_emitters; the call reports which one ran."""
+@pytest.mark.parametrize("name,scale", [("bos", 0.02), ("tomo", 0.003)])
+def test_default_variant_is_render_emitters(tracer, name, scale, monkeypatch):
+    """render_emitters is the default for every scene; the call reports which
+    kernel ran."""
     from paper_1812_05902_b200 import scenes
     monkeypatch.delenv("RAYBOS_K1", raising=False)
     scene, grid, info, desc = scenes.build(name, scale=scale)
     tracer.set_field(grid)
-    assert tracer.run_trace(scene, True, True).report["k1_kernel"] == code
+    assert tracer.run_trace(scene, True, True).report["k1_kernel"] == 1
