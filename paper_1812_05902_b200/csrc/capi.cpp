@@ -495,11 +495,14 @@ struct PartialOut {
 
 // CTAs per emitter (KScene::split).  Splitting an emitter's rays over several
 // CTAs keeps fewer distinct cones in flight, so the cells they read stay in
-// L2; each chunk costs one pilot and one tile flush.  The chunk is sized to
-// about 2e5 RK4 steps, estimating the steps per ray as the box depth along the
-// pupil axis over h, halved for emitters inside the box (measured optimum:
-// tomo 4-8, bos 24, 1024^3 flat from 48; bos +20%, 1024^3 +4%, tomo +1% over
-// one CTA per emitter).  Independently, a work list
+// L2; each chunk costs one pilot, one tile flush and a barrier wait for its
+// slowest warp.  The chunk is sized to about 1.25e6 RK4 steps, estimating the
+// steps per ray as the box depth along the pupil axis over h, halved for
+// emitters inside the box.  Measured optimum with the band-order patches
+// (scripts/gpu_ab_r02m.sh / r02n.sh): tomo 1 (+1.7% over 8), bos 4 (+1.7% over
+// 20), 1024^3 20-40 (one or two patch iterations per chunk; 5: -0.8%).  (With
+// the earlier coprime patch stride the optimum was 8 / 24 / 48: each chunk
+// then spanned the whole cone.)  Independently, a work list
 // shorter than the resident CTAs is split until every CTA gets two units (3
 // emitters x 4e6 rays: 1.29 s -> 17 ms), never below one patch iteration per
 // unit.  RAYBOS_SPLIT overrides.
@@ -529,7 +532,7 @@ int emitter_split(const rb_ctx* ctx, const rb_scene* s, const rbk::KScene& k, si
     for (int a = 0; a < 3; ++a) depth += std::fabs(ext[a] * ax[a]) / (an > 0.0 ? an : 1.0);
     // emitters inside the box (Tomo particles) trace half the depth on average
     const double steps = std::min<double>(depth / k.h * (1.0 - 0.5 * f_in), s->max_steps);
-    split = std::min(128.0, std::round(static_cast<double>(s->rays_per_source) * steps / 2e5));
+    split = std::min(128.0, std::round(static_cast<double>(s->rays_per_source) * steps / 1.25e6));
   }
   if (n_work > 0 && n_work < static_cast<size_t>(resident_ctas))
     split = std::max(split, std::ceil(2.0 * resident_ctas / static_cast<double>(n_work)));

@@ -209,7 +209,7 @@ def test_real_nccl_one_rank_job(monkeypatch, name):
 
 @pytest.mark.parametrize("name,scale", [("tomo", 0.005), ("bos", 0.02)])
 def test_bench_scene_on_three_devices_bit_identical(fake_nccl, name, scale):
-    """A bench scene with emitter splitting (tomo 8, bos 25 CTAs per emitter),
+    """A bench scene (bos: emitter splitting, 4 CTAs per emitter),
     the cell table and the shard-plan cache, on three in-process devices."""
     from paper_1812_05902_b200 import scenes
     from paper_1812_05902_b200.engine import GpuTracer
