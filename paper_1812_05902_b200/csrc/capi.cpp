@@ -339,6 +339,18 @@ int validate_scene(rb_ctx* ctx, const rb_scene* s) {
   return RB_OK;
 }
 
+// Rows per band of the warp patches (kernels.h): a CTA iteration's 8 patches
+// then cover a (256 / rows) x rows block of the pupil lattice.  Without a medium 4
+// (8x4 patches, the spot rows of a warp coincide); with one 8 (4x8 patches, a
+// 32x8 block per iteration instead of 64x4: 1024^3 +0.9%, tomo / bos +-0.1%;
+// 16: tomo -0.5%; scripts/gpu_ab_r02p.sh).  RAYBOS_BAND_ROWS = 4, 8 or 16 overrides.
+int band_rows(const rb_ctx* ctx, int with_field) {
+  if (!(with_field && ctx->has_field)) return 4;
+  int bh = 8;
+  if (const char* e = std::getenv("RAYBOS_BAND_ROWS")) bh = std::atoi(e);
+  return bh == 4 || bh == 16 ? bh : 8;
+}
+
 rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, int accumulate) {
   rbk::KScene k{};
   k.n_sources = s->n_sources;
@@ -353,9 +365,13 @@ rbk::KScene make_kscene(const rb_ctx* ctx, const rb_scene* s, int with_field, in
   k.sampling = s->sampling == RB_SAMPLING_STRATIFIED ? 0 : 1;
   {
     const int rows = (s->rays_per_source + k.cells - 1) / k.cells;
-    k.band_rays = 4 * k.cells;
-    const int64_t band_positions = static_cast<int64_t>((rows + 3) / 4) * k.band_rays;
-    k.patch_count = static_cast<int32_t>((band_positions + 31) / 32);
+    const int bh = band_rows(ctx, with_field);
+    k.band_h = bh;
+    k.band_sh = bh == 16 ? 4 : (bh == 8 ? 3 : 2);
+    k.band_rays = bh * k.cells;
+    k.band_full = rows / bh;
+    k.band_tail = rows - k.band_full * bh;
+    k.patch_count = static_cast<int32_t>((static_cast<int64_t>(rows) * k.cells + 31) / 32);
     const int warps = rbk::kBlock / 32;
     // Without a medium the unit's first patch iteration is its pilot, so a
     // coprime stride deals that iteration's 8 patches across the whole pupil

@@ -76,15 +76,20 @@ struct KScene {
   int32_t sampling;
   int32_t with_field;
   // warp patches: the pupil lattice (cells x rows, ray i = cy * cells + cx) is
-  // cut into bands of 4 rows, each enumerated column-major, so 32 consecutive
-  // band positions are a compact 8x4 block whose rays gather from the same
-  // few grid cells, and no lane idles where cells is not a multiple of 8 (only
-  // the warps that straddle two bands are split); patches are visited in a
-  // strided order so the first iteration (the tile pilot) samples the whole pupil.
-  int32_t band_rays;             // 4 * cells
+  // cut into bands of band_h rows (the last one band_tail rows), each
+  // enumerated column-major, so 32 consecutive band positions are a compact
+  // (32 / band_h) x band_h block whose rays gather from the same few grid cells,
+  // and no lane idles where cells is not a multiple of the block width (only
+  // the warps that straddle two bands are split); see make_kscene for the
+  // patch order.
+  int32_t band_rays;             // band_h * cells
   int32_t patch_count;
   int32_t patch_stride;          // coprime to patch_count
-  int32_t pad_patch;
+  int32_t band_h;                // rows per band: 4, 8 or 16
+  int32_t band_sh;               // log2(band_h)
+  int32_t band_full;             // bands of band_h rows
+  int32_t band_tail;             // rows of the last, partial band (0: none)
+  int32_t pad_band;
   // density grid (float4: n-1, dn/dx, dn/dy, dn/dz)
   const float4* grid;
   // optional per-cell coefficient table (nullptr = derive from the nodes)

@@ -391,10 +391,20 @@ __device__ __forceinline__ T warp_sum(T v) {
 // Ray index of `lane` in patch p of the band order (consecutive p are
 // neighbouring patches of the pupil lattice), or -1 past the lattice.
 __device__ __forceinline__ int patch_ray_at(const KScene& S, int p, int lane, int N) {
-  const int j = p * 32 + lane;  // position in the 4-row bands (kernels.h)
-  const int band = j / S.band_rays, rem = j - band * S.band_rays;
-  const int cx = rem >> 2, cy = band * 4 + (rem & 3);
-  return cy * S.cells + cx < N ? cy * S.cells + cx : -1;
+  const int j = p * 32 + lane;  // position in the bands (kernels.h)
+  const int band = j / S.band_rays;
+  int cx, cy;
+  if (band < S.band_full) {
+    const int rem = j - band * S.band_rays;
+    cx = rem >> S.band_sh;
+    cy = band * S.band_h + (rem & (S.band_h - 1));
+  } else {
+    if (S.band_tail == 0) return -1;
+    const int rem = j - S.band_full * S.band_rays;
+    cx = rem / S.band_tail;
+    cy = S.band_full * S.band_h + (rem - cx * S.band_tail);
+  }
+  return cx < S.cells && cy * S.cells + cx < N ? cy * S.cells + cx : -1;
 }
 
 // render_emitters' slot order: slot k kWarps + w (warp w, patch iteration k)
