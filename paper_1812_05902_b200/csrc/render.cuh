@@ -562,9 +562,9 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
     // (Taking the patches after the pilot from a shared counter instead, so
     // warps with short rays take more, measured no gain: the unit-end barrier
     // waits on the last ray's length, not on the patch count.)
-    // Straight pilot (field kernels): the unit's shared tile is placed from the
-    // first patch iteration's rays traced WITHOUT the medium (raygen + optics +
-    // sensor, ~1% of a ray through the field), so the CTA synchronises right
+    // Straight pilot (field kernels): the unit's shared tile is placed from one
+    // patch per warp, spread over the unit's iterations, traced WITHOUT the medium
+    // (raygen + optics + sensor, ~1% of a ray through the field), so the CTA synchronises right
     // after the unit starts instead of after its slowest warp's first ray has
     // crossed the volume (BOS: 2 patch iterations per unit, ~10% of warp time
     // was spent waiting at that barrier).  The medium only shifts spots by the
