@@ -77,8 +77,7 @@ typedef struct rb_surface {
 
 typedef struct rb_element {
   int32_t kind; /* RB_ELEM_* */
-  int32_t k1_kernel; /* out: the render kernel that ran: 1 render_emitters, 2 render_warps
-                        (0: no sources) */
+  int32_t reserved;
   /* aperture: center, axis = normal, radius.
    * thin lens: center, axis, focal_length, diameter. */
   rb_vec3 center;
@@ -136,8 +135,7 @@ typedef struct rb_scene {
  * (i,j,k) sits at origin + (i*dx, j*dy, k*dz), x-fastest storage. */
 typedef struct rb_field_desc {
   int32_t nx, ny, nz;
-  int32_t k1_kernel; /* out: the render kernel that ran: 1 render_emitters, 2 render_warps
-                        (0: no sources) */
+  int32_t reserved;
   rb_vec3 origin;
   rb_vec3 spacing;
 } rb_field_desc;
