@@ -158,7 +158,7 @@ typedef struct rb_trace_out {
   double wall_seconds;
   int32_t threads; /* devices used (RunReport::threads)                         */
   int32_t k1_kernel; /* out: the render kernel that ran: 1 render_emitters, 2 render_warps
-                        (0: no sources) */
+                        (0: no sources, or rb_trace_stats_fp64's validation kernel) */
   uint64_t config_hash;
   /* instrumentation (not in the reference report) */
   int64_t total_steps;     /* sum of RK4 steps over all rays                   */
