@@ -84,7 +84,7 @@ struct KScene {
   // patch order.
   int32_t band_rays;             // band_h * cells
   int32_t patch_count;
-  int32_t patch_stride;          // coprime to patch_count
+  int32_t patch_stride;          // coprime to patch_count (1 with a medium)
   int32_t band_h;                // rows per band: 4, 8 or 16
   int32_t band_sh;               // log2(band_h)
   int32_t band_full;             // bands of band_h rows

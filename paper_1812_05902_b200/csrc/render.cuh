@@ -556,8 +556,9 @@ __global__ void __launch_bounds__(kBlock, kField == 0 ? kMinBlocksNoField
     if (sh_work >= n_units) break;
     const int kb = (sh_work % S.split) * Kc, ke = min(K, kb + Kc);
 
-    // One loop, one trace_ray call site: iteration 0 is the pilot, after which
-    // the CTA places the tile.  __syncwarp() reconverges the lanes after every
+    // One loop, one trace_ray call site: without a medium iteration kb is the
+    // pilot, after which the CTA places the tile (with one, the straight pilot
+    // below places it first).  __syncwarp() reconverges the lanes after every
     // ray so a warp never splits into groups running different rays' RK4 loops.
     // (Taking the patches after the pilot from a shared counter instead, so
     // warps with short rays take more, measured no gain: the unit-end barrier
